@@ -1,0 +1,293 @@
+"""Pins for the CPU oracle (oracle/), independent of the oracle itself.
+
+Each pin is something the paper or mathematics fixes: closed forms, brute
+force on tiny inputs, invariants, textbook special cases.  Chosen so that a
+dropped term, a wrong sign/index or a transposed operand in any oracle mode
+fails at least one test.  CPU only (no GPU marker).
+"""
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from conftest import GOLDEN
+
+
+def golden_closed_forms():
+    out = {}
+    for line in open(os.path.join(GOLDEN, "closed_forms.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        k, v = line.split()
+        out[k] = int(v)
+    return out
+
+
+def brute_perm(A):
+    """Eq. 1 typed out independently with itertools (tiny n only)."""
+    n = A.shape[0]
+    return sum(math.prod(A[i, s[i]] for i in range(n)) for s in itertools.permutations(range(n)))
+
+
+def derangements(n):
+    d = [1, 0]
+    for k in range(2, n + 1):
+        d.append((k - 1) * (d[-1] + d[-2]))
+    return d[n]
+
+
+def fib(k):
+    a, b = 0, 1
+    for _ in range(k):
+        a, b = b, a + b
+    return a
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def nw_close(A, exact):
+    """long-double NW within its own error bound: |v - e| <= 4e-16 |e| (the
+    final rounding to double) + 1e-17 * sum|terms| (u = 2^-64 times the n+log
+    operation depth, cancellation-aware)."""
+    v, sabs = oracle.perm_nw(A)
+    return abs(v - exact) <= 4e-16 * abs(exact) + 1e-17 * sabs
+
+
+# ---- tiny brute force ------------------------------------------------------
+
+def test_2x2_closed_form():
+    A = np.array([[2.0, 3.0], [5.0, 7.0]])
+    assert oracle.perm_naive(A) == 2 * 7 + 3 * 5
+    assert oracle.perm_nw(A)[0] == 2 * 7 + 3 * 5
+    assert oracle.perm_ryser_exact(A) == 29
+    assert oracle.perm_nw_exact(A) == 29
+
+
+def test_3x3_written_out():
+    A = np.arange(1, 10, dtype=float).reshape(3, 3)
+    a = A
+    expect = (a[0, 0] * a[1, 1] * a[2, 2] + a[0, 0] * a[1, 2] * a[2, 1] + a[0, 1] * a[1, 0] * a[2, 2]
+              + a[0, 1] * a[1, 2] * a[2, 0] + a[0, 2] * a[1, 0] * a[2, 1] + a[0, 2] * a[1, 1] * a[2, 0])
+    assert expect == 450
+    for f in (oracle.perm_naive, lambda M: oracle.perm_nw(M)[0]):
+        assert f(A) == pytest.approx(450, rel=1e-15)
+    assert oracle.perm_ryser_exact(A) == 450
+    assert oracle.perm_nw_exact(A) == 450
+    assert oracle.perm_naive_exact(A) == 450
+
+
+def test_1x1():
+    A = np.array([[3.25]])
+    assert oracle.perm_naive(A) == 3.25
+    assert oracle.perm_nw(A)[0] == 3.25
+    assert oracle.perm_nw_exact(np.array([[-4]])) == -4
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_real_vs_brute(seed):
+    rng = np.random.default_rng(seed)
+    n = 3 + seed % 4
+    A = rng.uniform(-1, 1, (n, n)) * (rng.uniform(size=(n, n)) < 0.7)
+    b = brute_perm(A)
+    assert abs(oracle.perm_naive(A) - b) <= 1e-13 * abs(b) + 1e-300
+    v, sabs = oracle.perm_nw(A)
+    assert abs(v - b) <= 1e-15 * max(abs(b), sabs)
+
+
+# ---- closed forms ----------------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 2, 5, 8, 12, 16, 20])
+def test_identity(n):
+    I = np.eye(n)
+    assert oracle.perm_nw(I)[0] == pytest.approx(1.0, rel=1e-15)
+    assert oracle.perm_nw_exact(I) == 1
+    if n <= 10:
+        assert oracle.perm_naive(I) == 1.0
+    if n <= 12:
+        assert oracle.perm_ryser_exact(I) == 1
+    assert oracle.perm_band(I, 1) == 1.0
+
+
+@pytest.mark.parametrize("n", [2, 5, 8, 12, 16, 20])
+def test_all_ones_factorial(n):
+    J = np.ones((n, n))
+    assert oracle.perm_nw_exact(J) == math.factorial(n)
+    assert rel(oracle.perm_nw(J)[0], math.factorial(n)) < 1e-15
+    if n <= 9:
+        assert oracle.perm_naive_exact(J) == math.factorial(n)
+    if n <= 12:
+        assert oracle.perm_ryser_exact(J) == math.factorial(n)
+    if n == 20:
+        assert oracle.perm_nw_exact(J) == golden_closed_forms()["FACT20"]
+
+
+@pytest.mark.parametrize("n", [3, 6, 10, 14, 20])
+def test_derangements(n):
+    A = synth.derangement_matrix(n)
+    d = derangements(n)
+    assert oracle.perm_nw_exact(A) == d
+    assert rel(oracle.perm_nw(A)[0], d) < 1e-14
+    if n <= 10:
+        assert oracle.perm_naive_exact(A) == d
+        assert oracle.perm_ryser_exact(A) == d
+    g = golden_closed_forms()
+    if n == 10:
+        assert d == g["D10"]
+    if n == 20:
+        assert d == g["D20"]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 10, 20, 44])
+def test_tridiagonal_fibonacci(n):
+    A = synth.tridiagonal01(n)
+    f = fib(n + 1)
+    assert oracle.perm_band_exact(A, 1) == f
+    assert oracle.perm_band(A, 1) == float(f)
+    if n <= 20:
+        assert oracle.perm_nw_exact(A) == f
+        assert oracle.perm_nw(A)[0] == pytest.approx(f, rel=1e-15)
+    if n == 44:
+        assert f == golden_closed_forms()["F45"]
+
+
+def test_triangular_is_diagonal_product():
+    rng = np.random.default_rng(3)
+    n = 12
+    A = np.triu(rng.uniform(0.5, 2.0, (n, n)))
+    d = float(np.prod(np.diag(A)))
+    assert nw_close(A, d)
+    assert nw_close(A.T, d)
+
+
+def test_zero_row_gives_zero():
+    rng = np.random.default_rng(4)
+    A = rng.uniform(size=(9, 9))
+    A[4, :] = 0
+    assert oracle.perm_naive(A) == 0.0
+    assert abs(oracle.perm_nw(A)[0]) < 1e-12
+    assert oracle.structural_rank(A) == 8
+
+
+@pytest.mark.parametrize("n,b,seed", [(8, 4, 1), (16, 4, 2), (16, 8, 3), (24, 8, 4)])
+def test_block_rank1_closed_form(n, b, seed):
+    A, blocks = synth.block_rank1(n, b, seed)
+    cf = math.prod(math.factorial(b) * float(np.prod(u)) * float(np.prod(v)) for u, v in blocks)
+    assert rel(oracle.perm_nw(A)[0], cf) < 1e-13
+
+
+def test_block_diagonal_product():
+    rng = np.random.default_rng(11)
+    B1 = rng.uniform(size=(4, 4))
+    B2 = rng.uniform(size=(5, 5))
+    A = np.zeros((9, 9))
+    A[:4, :4] = B1
+    A[4:, 4:] = B2
+    assert rel(oracle.perm_nw(A)[0], brute_perm(B1) * brute_perm(B2)) < 1e-13
+
+
+# ---- cross-mode equalities on random inputs --------------------------------
+
+@pytest.mark.parametrize("seed", range(10))
+def test_integer_modes_agree(seed):
+    rng = np.random.default_rng(100 + seed)
+    n = 2 + seed % 8
+    A = rng.integers(-3, 4, (n, n)) * (rng.uniform(size=(n, n)) < 0.6)
+    e = oracle.perm_naive_exact(A)
+    assert oracle.perm_ryser_exact(A) == e
+    assert oracle.perm_nw_exact(A) == e
+    assert e == round(brute_perm(A.astype(float))) if n <= 7 else True
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_er_real_naive_vs_nw(seed):
+    n = 5 + seed % 5
+    A = synth.erdos_renyi(n, 0.3 + 0.05 * seed, seed)
+    assert rel(oracle.perm_nw(A)[0], oracle.perm_naive(A)) < 1e-13
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_band_dp_vs_naive(seed):
+    rng = np.random.default_rng(200 + seed)
+    n, w = 7 + seed % 3, 1 + seed % 3
+    A = rng.integers(1, 5, (n, n)).astype(float)
+    for i in range(n):
+        for j in range(n):
+            if abs(i - j) > w:
+                A[i, j] = 0
+    A[rng.uniform(size=(n, n)) < 0.2] = 0
+    assert oracle.perm_band_exact(A, w) == oracle.perm_naive_exact(A)
+    assert oracle.perm_band(A, w) == pytest.approx(oracle.perm_naive(A), rel=1e-15)
+
+
+def test_band_brickwork_matches_nw():
+    A = synth.givens_brickwork(20, 4, 7)
+    w = synth.half_bandwidth(A)
+    assert w <= 4
+    assert rel(oracle.perm_nw(A)[0], oracle.perm_band(A, w)) < 1e-12
+
+
+# ---- invariants ------------------------------------------------------------
+
+def test_permutation_and_transpose_invariance():
+    A = synth.erdos_renyi(14, 0.3, 5)
+    p = oracle.perm_nw(A)[0]
+    rng = np.random.default_rng(1)
+    P, Q = rng.permutation(14), rng.permutation(14)
+    assert rel(oracle.perm_nw(A[np.ix_(P, Q)])[0], p) < 1e-13
+    assert rel(oracle.perm_nw(A.T)[0], p) < 1e-13
+
+
+def test_multilinearity_in_a_row():
+    A = synth.erdos_renyi(12, 0.35, 6)
+    p = oracle.perm_nw(A)[0]
+    B = A.copy()
+    B[3] *= -2.5
+    assert rel(oracle.perm_nw(B)[0], -2.5 * p) < 1e-13
+
+
+def test_nw_range_additivity_and_scale():
+    A = synth.erdos_renyi(16, 0.3, 9)
+    n = 16
+    N = 1 << (n - 1)
+    total, _ = oracle.nw_range(A, 0, N)
+    a, _ = oracle.nw_range(A, 0, 12345)
+    b, _ = oracle.nw_range(A, 12345, N)
+    assert a + b == pytest.approx(total, rel=1e-12, abs=1e-12 * abs(total))
+    assert total * (4 * (n % 2) - 2) == pytest.approx(oracle.perm_naive(A) if n <= 10 else oracle.perm_nw(A)[0])
+
+
+def test_nw_exact_checksum_divisibility():
+    A = synth.erdos_renyi(12, 0.3, 2, binary=True)
+    T, zeros = oracle.nw2_range_exact(A, 0, 1 << 11)
+    assert T % (1 << 11) == 0
+    assert zeros > 0
+
+
+# ---- structural rank -------------------------------------------------------
+
+def brute_rank(A):
+    n = A.shape[0]
+    best = 0
+    for k in range(n, 0, -1):
+        for rows in itertools.combinations(range(n), k):
+            for cols in itertools.permutations(range(n), k):
+                if all(A[r, c] != 0 for r, c in zip(rows, cols)):
+                    return k
+    return best
+
+
+def test_structural_rank_cases():
+    assert oracle.structural_rank(np.eye(3)) == 3
+    A = np.zeros((3, 3))
+    A[:, 0] = 1
+    assert oracle.structural_rank(A) == 1
+    rng = np.random.default_rng(7)
+    for _ in range(6):
+        A = (rng.uniform(size=(5, 5)) < 0.3).astype(float)
+        assert oracle.structural_rank(A) == brute_rank(A)
