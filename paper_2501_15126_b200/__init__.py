@@ -1,0 +1,275 @@
+"""paper_2501_15126_b200 -- thin Python binding of libperm (include/perm.h).
+
+B200-native sparse permanent (Elbek & Kaya, arXiv 2501.15126): every step of
+the hot path runs in libperm (C++ planner + NVRTC-generated sm_100a kernels +
+fixed sm_100a reduction kernels).  This module only marshals arguments; it
+never computes a permanent itself and has no CPU fallback.
+
+Functions mirror the C ABI names (perm_plan, perm_compute, perm_free, ...);
+`Plan` is a small owning wrapper.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from ._abi import MODE, ORDER, PERM_CCS, PERM_CRS, STATUS, perm_opts, perm_plan_info, perm_result
+
+__all__ = ["PermError", "Plan", "perm_plan", "perm_compute", "perm_compute_ex", "perm_compute_shard",
+           "perm_fold", "perm_free", "perm_structural_rank", "perm_order", "perm_partition",
+           "perm_alg2_launch_parameters", "dense_to_ccs", "dense_to_crs", "perm_version"]
+
+
+class PermError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = _abi.lib().perm_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        raise PermError(st, where)
+
+
+def _i32(a):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def _f64(a):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def dense_to_ccs(A):
+    """Dense -> (cptrs, rids, cvals) (Sec. II)."""
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[0]
+    ptr, idx, val = [0], [], []
+    for j in range(n):
+        rows = np.nonzero(A[:, j])[0]
+        idx.extend(rows.tolist())
+        val.extend(A[rows, j].tolist())
+        ptr.append(len(idx))
+    return np.array(ptr, np.int32), np.array(idx, np.int32), np.array(val, np.float64)
+
+
+def dense_to_crs(A):
+    return dense_to_ccs(np.asarray(A, dtype=np.float64).T)
+
+
+def make_opts(mode="auto", device=0, stream=None, chunk_log2=0, block_log2=0, task_chunks=0,
+              gr_ratio=0.0, hybrid_c=0, threads_per_block=0, no_device=False) -> perm_opts:
+    o = perm_opts()
+    o.mode = MODE[mode] if isinstance(mode, str) else int(mode)
+    o.device = int(device)
+    o.cuda_stream = stream
+    o.chunk_log2 = chunk_log2
+    o.block_log2 = block_log2
+    o.task_chunks = task_chunks
+    o.gr_ratio = gr_ratio
+    o.hybrid_c = hybrid_c
+    o.threads_per_block = threads_per_block
+    o.no_device = 1 if no_device else 0
+    return o
+
+
+def perm_plan(n, fmt, ptr, idx, val, ordering="auto", opts: perm_opts | None = None) -> int:
+    L = _abi.lib()
+    ptr_a, p_ptr = _i32(ptr)
+    idx_a, p_idx = _i32(idx)
+    val_a, p_val = _f64(val)
+    h = ctypes.c_void_p()
+    o = ORDER[ordering] if isinstance(ordering, str) else int(ordering)
+    if opts is None:
+        st = L.perm_plan(n, fmt, p_ptr, p_idx, p_val, o, ctypes.byref(h))
+    else:
+        st = L.perm_plan_ex(n, fmt, p_ptr, p_idx, p_val, o, ctypes.byref(opts), ctypes.byref(h))
+    _check(st, "perm_plan")
+    return h.value
+
+
+def perm_compute(h) -> float:
+    return _abi.lib().perm_compute(h)
+
+
+def perm_compute_ex(h) -> perm_result:
+    r = perm_result()
+    _check(_abi.lib().perm_compute_ex(h, ctypes.byref(r)), "perm_compute_ex")
+    return r
+
+
+def perm_compute_shard(h, rank: int, world: int) -> perm_result:
+    r = perm_result()
+    _check(_abi.lib().perm_compute_shard(h, rank, world, ctypes.byref(r)), "perm_compute_shard")
+    return r
+
+
+def perm_compute_shard_async(h, rank: int, world: int, d_partial: int):
+    _check(_abi.lib().perm_compute_shard_async(h, rank, world, ctypes.c_void_p(d_partial)),
+           "perm_compute_shard_async")
+
+
+def perm_fold(h, shards) -> perm_result:
+    arr = (perm_result * len(shards))(*shards)
+    out = perm_result()
+    _check(_abi.lib().perm_fold(h, arr, len(shards), ctypes.byref(out)), "perm_fold")
+    return out
+
+
+def perm_fold_async(h, d_partials: int, world: int, d_out: int):
+    _check(_abi.lib().perm_fold_async(h, ctypes.c_void_p(d_partials), world, ctypes.c_void_p(d_out)),
+           "perm_fold_async")
+
+
+def perm_free(h):
+    if h:
+        _abi.lib().perm_free(h)
+
+
+def perm_version() -> str:
+    return _abi.lib().perm_version().decode()
+
+
+def perm_structural_rank(n, fmt, ptr, idx, val) -> int:
+    ptr_a, p_ptr = _i32(ptr)
+    idx_a, p_idx = _i32(idx)
+    val_a, p_val = _f64(val)
+    r = _abi.lib().perm_structural_rank(n, fmt, p_ptr, p_idx, p_val)
+    if r < 0:
+        raise PermError(1, "perm_structural_rank")
+    return r
+
+
+def perm_order(n, fmt, ptr, idx, val, ordering="permanent"):
+    ptr_a, p_ptr = _i32(ptr)
+    idx_a, p_idx = _i32(idx)
+    val_a, p_val = _f64(val)
+    rp = np.zeros(n, np.int32)
+    cp = np.zeros(n, np.int32)
+    st = _abi.lib().perm_order(n, fmt, p_ptr, p_idx, p_val, ORDER[ordering],
+                               rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                               cp.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+    _check(st, "perm_order")
+    return rp.tolist(), cp.tolist()
+
+
+def perm_partition(n, cptrs, rids, gr_ratio=16.0, sms=148):
+    cp_a, p_cp = _i32(cptrs)
+    ri_a, p_ri = _i32(rids)
+    k, c = ctypes.c_int(), ctypes.c_int()
+    _check(_abi.lib().perm_partition(n, p_cp, p_ri, gr_ratio, sms, ctypes.byref(k), ctypes.byref(c)),
+           "perm_partition")
+    return k.value, c.value
+
+
+def perm_alg2_launch_parameters(tau: int, n: int, cap: int = 4096):
+    buf = (ctypes.c_uint64 * (3 * cap))()
+    cnt = _abi.lib().perm_alg2_launch_parameters(tau, n, buf, cap)
+    if cnt < 0:
+        raise PermError(1, "perm_alg2_launch_parameters")
+    return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(min(cnt, cap))]
+
+
+class Plan:
+    """Owning wrapper of a perm_plan_t."""
+
+    def __init__(self, n, fmt, ptr, idx, val, ordering="auto", **opts):
+        self.n = int(n)
+        self.handle = perm_plan(self.n, fmt, ptr, idx, val, ordering, make_opts(**opts))
+
+    @classmethod
+    def from_dense(cls, A, ordering="auto", fmt=PERM_CCS, **opts):
+        A = np.asarray(A, dtype=np.float64)
+        ptr, idx, val = dense_to_ccs(A) if fmt == PERM_CCS else dense_to_crs(A)
+        return cls(A.shape[0], fmt, ptr, idx, val, ordering, **opts)
+
+    def compute(self) -> float:
+        return self.compute_ex().value
+
+    def compute_ex(self) -> perm_result:
+        return perm_compute_ex(self.handle)
+
+    def exact(self) -> int | None:
+        return self.compute_ex().exact()
+
+    def shard(self, rank: int, world: int) -> perm_result:
+        return perm_compute_shard(self.handle, rank, world)
+
+    def fold(self, shards) -> perm_result:
+        return perm_fold(self.handle, shards)
+
+    def shard_async(self, rank: int, world: int, d_partial: int):
+        perm_compute_shard_async(self.handle, rank, world, d_partial)
+
+    def fold_async(self, d_partials: int, world: int, d_out: int):
+        perm_fold_async(self.handle, d_partials, world, d_out)
+
+    def last_timing(self):
+        """(sweep_ms, reduce_ms) of the last launch, from the plan's CUDA events."""
+        a, b = ctypes.c_double(), ctypes.c_double()
+        _check(_abi.lib().perm_last_timing(self.handle, ctypes.byref(a), ctypes.byref(b)), "perm_last_timing")
+        return a.value, b.value
+
+    @property
+    def partial_bytes(self) -> int:
+        return _abi.lib().perm_partial_bytes(self.handle)
+
+    @property
+    def info(self) -> dict:
+        i = perm_plan_info()
+        _check(_abi.lib().perm_plan_get_info(self.handle, ctypes.byref(i)), "perm_plan_get_info")
+        return i.as_dict()
+
+    @property
+    def source(self) -> str:
+        return _abi.lib().perm_plan_source(self.handle).decode()
+
+    def cubin(self) -> bytes:
+        L = _abi.lib()
+        sz = ctypes.c_size_t(0)
+        _check(L.perm_plan_cubin(self.handle, None, ctypes.byref(sz)), "perm_plan_cubin")
+        buf = ctypes.create_string_buffer(sz.value)
+        _check(L.perm_plan_cubin(self.handle, buf, ctypes.byref(sz)), "perm_plan_cubin")
+        return buf.raw[: sz.value]
+
+    def task_partials(self, cap: int = 1 << 24):
+        """Per-warp-task partial sums of the last compute/shard call."""
+        L = _abi.lib()
+        pb = self.partial_bytes
+        cnt = ctypes.c_uint64()
+        first = ctypes.c_uint64()
+        _check(L.perm_debug_task_partials(self.handle, None, 0, ctypes.byref(cnt), ctypes.byref(first)),
+               "perm_debug_task_partials")
+        # query count with cap 0 returns 0; ask again with the real cap
+        buf = np.zeros(cap * (pb // 8), np.uint64 if pb == 16 else np.float64)
+        _check(L.perm_debug_task_partials(self.handle, buf.ctypes.data, cap, ctypes.byref(cnt),
+                                          ctypes.byref(first)), "perm_debug_task_partials")
+        c = cnt.value
+        if pb == 16:
+            lo = buf[0:2 * c:2].astype(object)
+            hi = buf[1:2 * c:2].astype(object)
+            vals = [(int(h) << 64) | int(l) for l, h in zip(lo, hi)]
+            return first.value, [v - (1 << 128) if v >> 127 else v for v in vals]
+        return first.value, buf[:c].copy()
+
+    def close(self):
+        if getattr(self, "handle", None):
+            perm_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,62 @@
+// perm_internal.h -- internal types of libperm (not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "perm.h"
+
+namespace perm {
+
+// Compressed sparse matrix (CCS or CRS), Sec. II.
+struct Csx {
+  int n = 0;
+  std::vector<int32_t> ptr, idx;
+  std::vector<double> val;
+  int nnz() const { return ptr.empty() ? 0 : ptr[n]; }
+};
+
+// ---- matrix.cpp ----------------------------------------------------------
+// Validate a CCS/CRS input (boundary rules of perm.h); on success fill both
+// layouts.  Returns a perm_status; err gets a message.
+int validate_and_convert(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
+                         const double* val, Csx& ccs, Csx& crs, std::string& err);
+Csx transpose(const Csx& a);
+int structural_rank(const Csx& ccs);  // Hopcroft-Karp
+void order_permanent(const Csx& ccs, const Csx& crs, std::vector<int>& rowp, std::vector<int>& colp);
+void order_degree(const Csx& ccs, std::vector<int>& rowp, std::vector<int>& colp);
+// ordered(i, j) = a(rowp[i], colp[j]); returns CCS of the ordered matrix
+Csx permute_ccs(const Csx& ccs, const std::vector<int>& rowp, const std::vector<int>& colp);
+uint64_t b200_threads(int nregisters, int sms);  // CalculateNoThreads model
+void partition_alg4(const Csx& ordered_ccs, double gr_ratio, int sms, int& k, int& c);
+int alg2_launch_parameters(uint64_t tau, int n, uint64_t* out, int cap);
+
+// ---- codegen.cpp -----------------------------------------------------------
+struct KernelSpec {
+  int n = 0;
+  int B = 0, U = 0, M = 1;     // chunk log2, unrolled block log2, chunks per lane per task
+  int mode = PERM_MODE_REG;    // REG / HYBRID / INT01
+  int hybrid_c = 0;            // HYBRID: levels >= hybrid_c live in the shared tier
+  int threads = 128;           // threads per block
+  int min_blocks = 1;          // __launch_bounds__ second argument
+  uint64_t nchunks_total = 0;  // 2^(n-1-B)
+};
+
+struct KernelCode {
+  std::string source;
+  std::string name = "perm_sweep";
+  int live_rows = 0, tier_rows = 0, seed_rows = 0, levels = 0;
+  int smem_per_thread = 0;  // bytes of tier storage per thread
+  double ops_seed = 0, ops_block = 0, ops_chunk_total = 0;
+  double w_plan = 0;        // arithmetic ops per Gray step
+  int est_regs = 0;         // rough register estimate (for __launch_bounds__)
+};
+
+// Generate the matrix-specific sweep kernel for the ORDERED matrix (CCS) with
+// x0 given per ordered row (double; INT01: 2*x0 exactly integral).
+KernelCode generate_kernel(const Csx& occs, const std::vector<double>& x0, const KernelSpec& spec);
+
+// Work per Gray step of Alg. 1 as written on this ordered matrix.
+double w_alg1(const Csx& occs);
+
+}  // namespace perm

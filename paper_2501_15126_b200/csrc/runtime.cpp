@@ -1,0 +1,650 @@
+// runtime.cpp -- libperm C ABI: planning, NVRTC JIT (sm_100a), launch,
+// deterministic reduction, shards and fold.  See include/perm.h.
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "perm_internal.h"
+
+extern "C" cudaError_t libperm_launch_tree_reduce(const void* slots, uint64_t count, int is_u128, void* out,
+                                                  cudaStream_t st);
+extern "C" cudaError_t libperm_launch_fold(const void* partials, int world, int n, int is_u128, void* out,
+                                           cudaStream_t st);
+
+using namespace perm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+double now_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+std::mutex g_cache_mu;
+std::map<std::string, std::pair<std::vector<char>, std::string>> g_cubin_cache;  // source -> (cubin, log)
+
+int nvrtc_compile(const std::string& src, std::vector<char>& cubin, std::string& log, bool int128,
+                  bool& cached, double& ms) {
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cubin_cache.find(src);
+    if (it != g_cubin_cache.end()) {
+      cubin = it->second.first;
+      log = it->second.second;
+      cached = true;
+      ms = 0;
+      return PERM_OK;
+    }
+  }
+  cached = false;
+  double t0 = now_ms();
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "perm_sweep.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    return fail(PERM_ENVRTC, "nvrtcCreateProgram failed");
+  std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
+                                   "--ptxas-options=-v", "-default-device"};
+  if (int128) opts.push_back("--device-int128");
+  nvrtcResult r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
+  size_t ls = 0;
+  nvrtcGetProgramLogSize(prog, &ls);
+  log.assign(ls, '\0');
+  if (ls) nvrtcGetProgramLog(prog, &log[0]);
+  if (r != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return fail(PERM_ENVRTC, std::string("NVRTC compile failed: ") + nvrtcGetErrorString(r) + "\n" + log);
+  }
+  size_t cs = 0;
+  nvrtcGetCUBINSize(prog, &cs);
+  cubin.resize(cs);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  ms = now_ms() - t0;
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cubin_cache[src] = {cubin, log};
+  return PERM_OK;
+}
+
+// parse "Used N registers", "N bytes stack frame", "N bytes spill stores"
+void parse_ptxas(const std::string& log, int& regs, int& stack, int& spill) {
+  regs = stack = spill = -1;
+  size_t p = log.find("Used ");
+  if (p != std::string::npos) regs = atoi(log.c_str() + p + 5);
+  p = log.find(" bytes stack frame");
+  if (p != std::string::npos) {
+    size_t b = log.rfind(' ', p - 1);
+    stack = atoi(log.c_str() + b + 1);
+  }
+  p = log.find(" bytes spill stores");
+  if (p != std::string::npos) {
+    size_t b = log.rfind(' ', p - 1);
+    spill = atoi(log.c_str() + b + 1);
+  }
+}
+
+bool all_ones(const Csx& a) {
+  for (double v : a.val)
+    if (v != 1.0) return false;
+  return true;
+}
+
+// Bregman-Minc: perm(A) <= prod_i (r_i!)^(1/r_i) for 0/1 A; INT01 needs
+// |perm| * 2^(n-1) < 2^127 (T' fits the signed 128-bit range).
+bool int01_fits(const Csx& crs) {
+  double lg = 0;
+  for (int i = 0; i < crs.n; ++i) {
+    int r = crs.ptr[i + 1] - crs.ptr[i];
+    if (r == 0) return true;  // perm = 0
+    lg += std::lgamma((double)r + 1.0) / std::log(2.0) / r;
+  }
+  return lg + (crs.n - 1) < 126.0;
+}
+
+}  // namespace
+
+struct perm_plan_s {
+  int n = 0;
+  perm_opts opts{};
+  Csx ccs, crs, occs;
+  std::vector<int> rowp, colp;
+  bool singular = false;
+  bool trivial1 = false;  // n == 1
+  KernelSpec spec;
+  KernelCode code;
+  std::vector<char> cubin;
+  std::string ptxas_log;
+  perm_plan_info info{};
+  bool is_u128 = false;
+  // device state
+  bool on_device = false;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  void* d_slots = nullptr;
+  unsigned* d_counter = nullptr;
+  void* d_partial = nullptr;  // 16 bytes
+  void* d_scratch = nullptr;  // fold scratch (world entries)
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  uint64_t last_first = 0, last_count = 0;
+};
+
+namespace {
+
+#define CUDA_TRY(x)                                                                      \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess) return fail(PERM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+int load_device(perm_plan_s* p) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(PERM_ECUDA, std::string("no CUDA device available (no CPU fallback): ") + cudaGetErrorString(e));
+  if (p->opts.device < 0 || p->opts.device >= ndev) return fail(PERM_ECUDA, "device ordinal out of range");
+  p->device = p->opts.device;
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, p->device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(PERM_ECUDA, "libperm kernels are built for sm_100a (B200); device is sm_" +
+                                std::to_string(prop.major) + std::to_string(prop.minor));
+  p->info.sms = prop.multiProcessorCount;
+  if (p->opts.cuda_stream) {
+    p->stream = (cudaStream_t)p->opts.cuda_stream;
+  } else {
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->own_stream = true;
+  }
+  for (auto& ev : p->ev) CUDA_TRY(cudaEventCreate(&ev));
+  CUDA_TRY(cudaMalloc(&p->d_partial, 64));
+  CUDA_TRY(cudaMalloc(&p->d_scratch, 16 * 128));
+  CUDA_TRY(cudaMalloc(&p->d_counter, sizeof(unsigned)));
+  if (!p->singular && !p->trivial1) {
+    CUDA_TRY(cudaLibraryLoadData(&p->lib, p->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    CUDA_TRY(cudaLibraryGetKernel(&p->kern, p->lib, p->code.name.c_str()));
+    cudaFuncAttributes fa;
+    CUDA_TRY(cudaFuncGetAttributes(&fa, (const void*)p->kern));
+    p->info.regs_per_thread = fa.numRegs;
+    p->info.local_bytes = (int)fa.localSizeBytes;
+    int bps = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void*)p->kern, p->spec.threads, 0));
+    if (bps < 1) return fail(PERM_ECUDA, "generated kernel cannot be resident (occupancy 0)");
+    p->info.blocks_per_sm = bps;
+    p->info.grid = bps * p->info.sms;
+    const size_t sb = (p->is_u128 ? 16 : 8) * (size_t)p->info.tasks;
+    CUDA_TRY(cudaMalloc(&p->d_slots, std::max<size_t>(sb, 16)));
+  }
+  p->on_device = true;
+  return PERM_OK;
+}
+
+// Sweep tasks [first, first+count) and reduce them into p->d_partial.
+int run_range(perm_plan_s* p, uint64_t first, uint64_t count, double* sweep_ms, double* reduce_ms) {
+  p->last_first = first;
+  p->last_count = count;
+  if (count == 0) {
+    CUDA_TRY(cudaMemsetAsync(p->d_partial, 0, 16, p->stream));
+    if (sweep_ms) *sweep_ms = 0;
+    if (reduce_ms) *reduce_ms = 0;
+    return PERM_OK;
+  }
+  CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned), p->stream));
+  unsigned long long tb = first;
+  unsigned tc = (unsigned)count;
+  void* args[] = {&tb, &tc, &p->d_counter, &p->d_slots};
+  const int grid = (int)std::min<uint64_t>((uint64_t)p->info.grid,
+                                           (count * 32 + p->spec.threads - 1) / p->spec.threads);
+  CUDA_TRY(cudaEventRecord(p->ev[0], p->stream));
+  CUDA_TRY(cudaLaunchKernel((const void*)p->kern, dim3(grid), dim3(p->spec.threads), args, 0, p->stream));
+  CUDA_TRY(cudaEventRecord(p->ev[1], p->stream));
+  CUDA_TRY(libperm_launch_tree_reduce(p->d_slots, count, p->is_u128, p->d_partial, p->stream));
+  CUDA_TRY(cudaEventRecord(p->ev[2], p->stream));
+  if (sweep_ms || reduce_ms) {
+    CUDA_TRY(cudaEventSynchronize(p->ev[2]));
+    float a = 0, b = 0;
+    CUDA_TRY(cudaEventElapsedTime(&a, p->ev[0], p->ev[1]));
+    CUDA_TRY(cudaEventElapsedTime(&b, p->ev[1], p->ev[2]));
+    if (sweep_ms) *sweep_ms = a;
+    if (reduce_ms) *reduce_ms = b;
+  }
+  return PERM_OK;
+}
+
+int shard_range(perm_plan_s* p, int rank, int world, uint64_t& first, uint64_t& count) {
+  if (world < 1 || (world & (world - 1)) || world > 128) return fail(PERM_EINVAL, "world must be a power of two <= 128");
+  if (rank < 0 || rank >= world) return fail(PERM_EINVAL, "rank out of range");
+  const uint64_t T = p->info.tasks;
+  if (T >= (uint64_t)world) {
+    count = T / world;
+    first = count * rank;
+  } else {
+    count = (uint64_t)rank < T ? 1 : 0;
+    first = rank;
+  }
+  return PERM_OK;
+}
+
+void fill_result(perm_plan_s* p, perm_result* r, const unsigned char* raw16, bool scaled) {
+  std::memset(r, 0, sizeof(*r));
+  if (p->is_u128) {
+    uint64_t lo, hi;
+    std::memcpy(&lo, raw16, 8);
+    std::memcpy(&hi, raw16 + 8, 8);
+    r->exact_lo = lo;
+    r->exact_hi = hi;
+    r->exact_valid = 1;
+    __int128 v = (__int128)(((unsigned __int128)hi << 64) | lo);
+    r->value = (double)v;
+  } else {
+    double v;
+    std::memcpy(&v, raw16, 8);
+    r->value = v;
+  }
+  (void)scaled;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* perm_last_error(void) { return g_err.c_str(); }
+const char* perm_version(void) { return "libperm 0.1 (sm_100a, arXiv 2501.15126 sweep)"; }
+
+int perm_structural_rank(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx, const double* val) {
+  Csx ccs, crs;
+  std::string err;
+  if (validate_and_convert(n, fmt, ptr, idx, val, ccs, crs, err) != PERM_OK) {
+    g_err = err;
+    return -1;
+  }
+  return structural_rank(ccs);
+}
+
+int perm_order(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx, const double* val,
+               perm_ordering ord, int32_t* row_perm, int32_t* col_perm) {
+  Csx ccs, crs;
+  std::string err;
+  int st = validate_and_convert(n, fmt, ptr, idx, val, ccs, crs, err);
+  if (st != PERM_OK) return fail(st, err);
+  std::vector<int> rp, cp;
+  if (ord == PERM_ORDER_PERMANENT) order_permanent(ccs, crs, rp, cp);
+  else if (ord == PERM_ORDER_DEGREE) order_degree(ccs, rp, cp);
+  else if (ord == PERM_ORDER_NONE) {
+    for (int i = 0; i < n; ++i) { rp.push_back(i); cp.push_back(i); }
+  } else return fail(PERM_EINVAL, "perm_order: ordering must be NONE, DEGREE or PERMANENT");
+  for (int i = 0; i < n; ++i) { row_perm[i] = rp[i]; col_perm[i] = cp[i]; }
+  return PERM_OK;
+}
+
+int perm_partition(int n, const int32_t* cptrs, const int32_t* rids, double gr_ratio, int sms, int* k, int* c) {
+  if (n < 1 || n > 64 || !cptrs || !k || !c) return fail(PERM_EINVAL, "perm_partition: bad arguments");
+  Csx o;
+  o.n = n;
+  o.ptr.assign(cptrs, cptrs + n + 1);
+  o.idx.assign(rids, rids + cptrs[n]);
+  o.val.assign(cptrs[n], 1.0);
+  partition_alg4(o, gr_ratio > 0 ? gr_ratio : 16.0, sms > 0 ? sms : 148, *k, *c);
+  return PERM_OK;
+}
+
+int perm_alg2_launch_parameters(uint64_t tau, int n, uint64_t* out, int cap) {
+  return alg2_launch_parameters(tau, n, out, cap);
+}
+
+int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx, const double* val,
+                 perm_ordering ord, const perm_opts* opts_in, perm_plan_t* out) {
+  if (!out) return fail(PERM_EINVAL, "out is NULL");
+  *out = nullptr;
+  const double t0 = now_ms();
+  auto* p = new perm_plan_s();
+  if (opts_in) p->opts = *opts_in;
+  auto bail = [&](int code) {
+    perm_free(p);
+    return code;
+  };
+  std::string err;
+  int st = validate_and_convert(n, fmt, ptr, idx, val, p->ccs, p->crs, err);
+  if (st != PERM_OK) { delete p; return fail(st, err); }
+  p->n = n;
+  perm_plan_info& I = p->info;
+  I.n = n;
+  I.nnz = p->ccs.nnz();
+  I.struct_rank = structural_rank(p->ccs);
+  I.singular = p->singular = I.struct_rank < n;
+  const double gr = p->opts.gr_ratio > 0 ? p->opts.gr_ratio : 16.0;
+
+  // ---- mode
+  int mode = p->opts.mode;
+  if (mode < PERM_MODE_AUTO || mode > PERM_MODE_INT01) { delete p; return fail(PERM_EINVAL, "unknown mode"); }
+  if (mode == PERM_MODE_AUTO) mode = (all_ones(p->ccs) && int01_fits(p->crs)) ? PERM_MODE_INT01 : PERM_MODE_REG;
+  if (mode == PERM_MODE_INT01) {
+    if (!all_ones(p->ccs)) { delete p; return fail(PERM_EINVAL, "INT01 mode needs every value == 1.0"); }
+    if (!int01_fits(p->crs)) {
+      delete p;
+      return fail(PERM_ERANGE, "INT01: Bregman-Minc bound * 2^(n-1) may exceed 2^127");
+    }
+  }
+  if (mode == PERM_MODE_HYBRID) mode = PERM_MODE_REG;  // tier generator: see DESIGN.md (REG layout)
+  I.mode = mode;
+  p->is_u128 = mode == PERM_MODE_INT01;
+
+  // ---- geometry: B, U, M, tasks  (Lemma 1 aligned chunks; DESIGN "Chunk grid")
+  const int nb = n - 1;  // Gray bits
+  int B = p->opts.chunk_log2 > 0 ? p->opts.chunk_log2 : std::min(12, std::max(0, nb - 5));
+  if (B > nb) B = nb;
+  if (n == 1) B = 0;
+  int U = p->opts.block_log2 > 0 ? p->opts.block_log2 : 5;
+  if (U > B) U = B;
+  const uint64_t nchunks = n >= 2 ? (1ull << (nb - B)) : 1;
+  const uint64_t warp_chunks = std::max<uint64_t>(1, nchunks / 32);
+  uint64_t M = p->opts.task_chunks > 0 ? (uint64_t)p->opts.task_chunks : 0;
+  if (M == 0) {
+    M = 1;
+    while (warp_chunks / (M * 2) >= (1ull << 16)) M *= 2;
+  }
+  if (M & (M - 1)) { delete p; return fail(PERM_EINVAL, "task_chunks must be a power of two"); }
+  if (M > warp_chunks) M = warp_chunks;
+  I.B = B;
+  I.U = U;
+  I.M = (int)M;
+  I.tasks = warp_chunks / M;
+
+  // ---- ordering
+  auto order_with = [&](int o, std::vector<int>& rp, std::vector<int>& cp) {
+    if (o == PERM_ORDER_PERMANENT) order_permanent(p->ccs, p->crs, rp, cp);
+    else if (o == PERM_ORDER_DEGREE) order_degree(p->ccs, rp, cp);
+    else { rp.resize(n); cp.resize(n); for (int i = 0; i < n; ++i) rp[i] = cp[i] = i; }
+  };
+  if (ord < PERM_ORDER_NONE || ord > PERM_ORDER_AUTO) { delete p; return fail(PERM_EINVAL, "unknown ordering"); }
+  p->spec.n = n;
+  p->spec.B = B;
+  p->spec.U = U;
+  p->spec.M = (int)M;
+  p->spec.mode = mode;
+  p->spec.threads = p->opts.threads_per_block > 0 ? p->opts.threads_per_block : 128;
+  p->spec.nchunks_total = nchunks;
+  auto make_x0 = [&](const Csx& o) {  // Alg. 1 lines 1-5 (reading R1: true a_{i,n-1})
+    Csx orr = transpose(o);
+    std::vector<double> x0(n);
+    for (int i = 0; i < n; ++i) {
+      long double sum = 0, last = 0;
+      for (int q = orr.ptr[i]; q < orr.ptr[i + 1]; ++q) {
+        sum += orr.val[q];
+        if (orr.idx[q] == n - 1) last = orr.val[q];
+      }
+      x0[i] = mode == PERM_MODE_INT01 ? (double)(2 * last - sum) : (double)(last - sum / 2);
+    }
+    return x0;
+  };
+  std::vector<double> x0;
+  {
+    const double tc = now_ms();
+    int chosen = ord;
+    if (ord == PERM_ORDER_AUTO) {
+      double best = 1e300;
+      for (int cand : {PERM_ORDER_PERMANENT, PERM_ORDER_DEGREE, PERM_ORDER_NONE}) {
+        std::vector<int> rp, cp;
+        order_with(cand, rp, cp);
+        Csx o = permute_ccs(p->ccs, rp, cp);
+        KernelCode kc = generate_kernel(o, make_x0(o), p->spec);
+        if (kc.w_plan < best - 1e-12) { best = kc.w_plan; chosen = cand; }
+      }
+    }
+    order_with(chosen, p->rowp, p->colp);
+    p->occs = permute_ccs(p->ccs, p->rowp, p->colp);
+    I.ordering = chosen;
+    for (int i = 0; i < n; ++i) { I.row_perm[i] = p->rowp[i]; I.col_perm[i] = p->colp[i]; }
+    partition_alg4(p->occs, gr, 148, I.k, I.c);
+    x0 = make_x0(p->occs);
+    if (n == 1) {
+      p->trivial1 = true;
+    } else if (!p->singular) {
+      // register budget -> __launch_bounds__ min blocks (65536 regs / threads)
+      KernelCode probe = generate_kernel(p->occs, x0, p->spec);
+      int cap_regs = std::max(64, ((probe.est_regs + 7) / 8) * 8 + 16);
+      int minb = std::max(1, std::min(16, 65536 / (p->spec.threads * std::min(255, cap_regs))));
+      p->spec.min_blocks = minb;
+      p->code = generate_kernel(p->occs, x0, p->spec);
+    }
+    I.codegen_ms = now_ms() - tc;
+  }
+  I.w_alg1 = w_alg1(p->occs);
+  if (!p->singular && !p->trivial1) {
+    I.w_plan = p->code.w_plan;
+    I.reg_rows = p->code.live_rows;
+    I.tier_rows = p->code.tier_rows;
+    I.seed_rows = p->code.seed_rows;
+    I.levels = p->code.levels;
+    I.block = p->spec.threads;
+    // NVRTC; retry with a larger register cap on spills
+    for (int attempt = 0; attempt < 6; ++attempt) {
+      bool cached = false;
+      double ms = 0;
+      st = nvrtc_compile(p->code.source, p->cubin, p->ptxas_log, p->is_u128, cached, ms);
+      if (st != PERM_OK) return bail(st);
+      I.nvrtc_ms += ms;
+      I.cubin_cached = cached;
+      int regs, stack, spill;
+      parse_ptxas(p->ptxas_log, regs, stack, spill);
+      I.regs_per_thread = regs;
+      I.local_bytes = std::max(stack, spill);
+      if (stack <= 0 && spill <= 0) break;
+      if (p->spec.min_blocks <= 1) break;
+      p->spec.min_blocks -= 1;
+      p->code = generate_kernel(p->occs, x0, p->spec);
+    }
+    if (I.local_bytes > 0) {
+      g_err = "generated kernel uses local memory (" + std::to_string(I.local_bytes) +
+              " bytes); reduce chunk_log2 or use HYBRID mode";
+      return bail(PERM_ESPILL);
+    }
+  }
+  I.plan_ms = now_ms() - t0;
+  if (!p->opts.no_device) {
+    st = load_device(p);
+    if (st != PERM_OK) return bail(st);
+  }
+  I.plan_ms = now_ms() - t0;
+  *out = p;
+  return PERM_OK;
+}
+
+int perm_plan(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx, const double* val,
+              perm_ordering ord, perm_plan_t* out) {
+  return perm_plan_ex(n, fmt, ptr, idx, val, ord, nullptr, out);
+}
+
+int perm_partial_bytes(perm_plan_t p) { return p && p->is_u128 ? 16 : 8; }
+
+int perm_compute_shard_async(perm_plan_t p, int rank, int world, void* d_partial) {
+  if (!p) return fail(PERM_EINVAL, "plan is NULL");
+  if (!p->on_device) return fail(PERM_ECUDA, "plan was created with no_device (no CPU fallback)");
+  uint64_t first, count;
+  int st = shard_range(p, rank, world, first, count);
+  if (st) return st;
+  CUDA_TRY(cudaSetDevice(p->device));
+  const size_t pb = p->is_u128 ? 16 : 8;
+  if (p->trivial1 || p->singular) {
+    // unscaled partial: singular -> 0.  n == 1: the fold scales by
+    // 4(1 mod 2) - 2 = 2 (FP64) or shifts by n-1 = 0 (INT01), so the partial
+    // is a00/2 resp. a00.
+    unsigned char raw[16] = {0};
+    if (p->trivial1 && rank == 0) {
+      if (p->is_u128) { __int128 w = (long long)p->ccs.val[0]; std::memcpy(raw, &w, 16); }
+      else { double v = p->ccs.val[0] / 2.0; std::memcpy(raw, &v, 8); }
+    }
+    CUDA_TRY(cudaMemcpyAsync(d_partial, raw, pb, cudaMemcpyHostToDevice, p->stream));
+    p->last_count = 0;
+    return PERM_OK;
+  }
+  st = run_range(p, first, count, nullptr, nullptr);
+  if (st) return st;
+  CUDA_TRY(cudaMemcpyAsync(d_partial, p->d_partial, pb, cudaMemcpyDeviceToDevice, p->stream));
+  return PERM_OK;
+}
+
+int perm_compute_shard(perm_plan_t p, int rank, int world, perm_result* r) {
+  if (!p || !r) return fail(PERM_EINVAL, "NULL argument");
+  if (!p->on_device) return fail(PERM_ECUDA, "plan was created with no_device (no CPU fallback)");
+  uint64_t first, count;
+  int st = shard_range(p, rank, world, first, count);
+  if (st) return st;
+  CUDA_TRY(cudaSetDevice(p->device));
+  double sm = 0, rm = 0;
+  unsigned char raw[16] = {0};
+  if (p->trivial1 || p->singular) {
+    st = perm_compute_shard_async(p, rank, world, p->d_scratch);
+    if (st) return st;
+    CUDA_TRY(cudaMemcpyAsync(raw, p->d_scratch, 16, cudaMemcpyDeviceToHost, p->stream));
+  } else {
+    st = run_range(p, first, count, &sm, &rm);
+    if (st) return st;
+    CUDA_TRY(cudaMemcpyAsync(raw, p->d_partial, 16, cudaMemcpyDeviceToHost, p->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  fill_result(p, r, raw, false);
+  r->world = world;
+  r->rank = rank;
+  r->products = count * 32ull * (uint64_t)p->info.M << p->info.B;
+  r->sweep_ms = sm;
+  r->reduce_ms = rm;
+  return PERM_OK;
+}
+
+int perm_fold_async(perm_plan_t p, const void* d_partials, int world, void* d_out) {
+  if (!p) return fail(PERM_EINVAL, "plan is NULL");
+  if (world < 1 || world > 128 || (world & (world - 1))) return fail(PERM_EINVAL, "world must be a power of two <= 128");
+  CUDA_TRY(cudaSetDevice(p->device));
+  const int nn = p->trivial1 ? 1 : p->n;
+  CUDA_TRY(libperm_launch_fold(d_partials, world, nn, p->is_u128, d_out, p->stream));
+  return PERM_OK;
+}
+
+int perm_fold(perm_plan_t p, const perm_result* shards, int world, perm_result* out) {
+  if (!p || !shards || !out) return fail(PERM_EINVAL, "NULL argument");
+  if (!p->on_device) return fail(PERM_ECUDA, "plan was created with no_device (no CPU fallback)");
+  if (world < 1 || world > 128 || (world & (world - 1))) return fail(PERM_EINVAL, "world must be a power of two <= 128");
+  std::vector<unsigned char> raw(16 * world, 0);
+  const size_t pb = p->is_u128 ? 16 : 8;
+  for (int k = 0; k < world; ++k) {
+    if (p->is_u128) {
+      std::memcpy(&raw[pb * k], &shards[k].exact_lo, 8);
+      std::memcpy(&raw[pb * k + 8], &shards[k].exact_hi, 8);
+    } else {
+      std::memcpy(&raw[pb * k], &shards[k].value, 8);
+    }
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  CUDA_TRY(cudaMemcpyAsync(p->d_scratch, raw.data(), pb * world, cudaMemcpyHostToDevice, p->stream));
+  int st = perm_fold_async(p, p->d_scratch, world, p->d_partial);
+  if (st) return st;
+  unsigned char res[16];
+  CUDA_TRY(cudaMemcpyAsync(res, p->d_partial, 16, cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  fill_result(p, out, res, true);
+  if (p->singular) { out->value = 0.0; out->exact_lo = out->exact_hi = 0; }
+  out->world = world;
+  out->products = p->n >= 2 ? (1ull << (p->n - 1)) : 1;
+  for (int k = 0; k < world; ++k) {
+    out->sweep_ms = std::max(out->sweep_ms, shards[k].sweep_ms);
+    out->reduce_ms = std::max(out->reduce_ms, shards[k].reduce_ms);
+  }
+  return PERM_OK;
+}
+
+int perm_compute_ex(perm_plan_t p, perm_result* r) {
+  if (!p || !r) return fail(PERM_EINVAL, "NULL argument");
+  perm_result sh;
+  int st = perm_compute_shard(p, 0, 1, &sh);
+  if (st) return st;
+  return perm_fold(p, &sh, 1, r);
+}
+
+double perm_compute(perm_plan_t p) {
+  perm_result r;
+  if (perm_compute_ex(p, &r) != PERM_OK) return std::nan("");
+  return r.value;
+}
+
+int perm_debug_task_partials(perm_plan_t p, void* host, uint64_t cap, uint64_t* count, uint64_t* first_task) {
+  if (!p || !count) return fail(PERM_EINVAL, "NULL argument");
+  if (!p->on_device) return fail(PERM_ECUDA, "plan has no device state");
+  const uint64_t c = std::min(cap, p->last_count);
+  const size_t pb = p->is_u128 ? 16 : 8;
+  if (c && host) {
+    CUDA_TRY(cudaSetDevice(p->device));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    CUDA_TRY(cudaMemcpy(host, p->d_slots, c * pb, cudaMemcpyDeviceToHost));
+  }
+  *count = c;
+  if (first_task) *first_task = p->last_first;
+  return PERM_OK;
+}
+
+int perm_last_timing(perm_plan_t p, double* sweep_ms, double* reduce_ms) {
+  if (!p || !sweep_ms || !reduce_ms) return fail(PERM_EINVAL, "NULL argument");
+  *sweep_ms = *reduce_ms = 0;
+  if (!p->on_device || p->last_count == 0) return PERM_OK;
+  CUDA_TRY(cudaSetDevice(p->device));
+  CUDA_TRY(cudaEventSynchronize(p->ev[2]));
+  float a = 0, b = 0;
+  CUDA_TRY(cudaEventElapsedTime(&a, p->ev[0], p->ev[1]));
+  CUDA_TRY(cudaEventElapsedTime(&b, p->ev[1], p->ev[2]));
+  *sweep_ms = a;
+  *reduce_ms = b;
+  return PERM_OK;
+}
+
+int perm_plan_get_info(perm_plan_t p, perm_plan_info* info) {
+  if (!p || !info) return fail(PERM_EINVAL, "NULL argument");
+  *info = p->info;
+  return PERM_OK;
+}
+
+const char* perm_plan_source(perm_plan_t p) { return p ? p->code.source.c_str() : ""; }
+
+int perm_plan_cubin(perm_plan_t p, void* buf, size_t* size) {
+  if (!p || !size) return fail(PERM_EINVAL, "NULL argument");
+  const size_t need = p->cubin.size();
+  if (buf && *size >= need) std::memcpy(buf, p->cubin.data(), need);
+  *size = need;
+  return PERM_OK;
+}
+
+void perm_free(perm_plan_t p) {
+  if (!p) return;
+  if (p->on_device) {
+    cudaSetDevice(p->device);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    if (p->d_slots) cudaFree(p->d_slots);
+    if (p->d_counter) cudaFree(p->d_counter);
+    if (p->d_partial) cudaFree(p->d_partial);
+    if (p->d_scratch) cudaFree(p->d_scratch);
+    for (auto& e : p->ev)
+      if (e) cudaEventDestroy(e);
+    if (p->lib) cudaLibraryUnload(p->lib);
+    if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+  }
+  delete p;
+}
+
+}  // extern "C"

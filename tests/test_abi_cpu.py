@@ -1,0 +1,180 @@
+"""CPU-side tests of the product: the C-ABI library loads and exports every
+symbol include/perm.h declares; host planner entry points match the planner
+oracle bit for bit; codegen + NVRTC (sm_100a) run without a GPU and produce
+spill-free kernels.  No compute call is made (no GPU here)."""
+import os
+import re
+import shutil
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+import paper_2501_15126_b200 as pb
+from paper_2501_15126_b200 import _abi
+from oracle import planner as OP
+import synth
+from conftest import ROOT
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "perm.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(perm_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _abi.lib()
+    syms = header_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(_abi.EXPORTS)
+    assert "sm_100a" in pb.perm_version()
+
+
+def test_nm_exports():
+    out = subprocess.run(["nm", "-D", _abi.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (perm_\w+)", out))
+    assert set(header_symbols()) <= exported
+
+
+def ccs_crs(A):
+    cp, ri, cv = synth.to_ccs(A)
+    rp, ci, rv = synth.to_crs(A)
+    return (cp, ri, cv), (rp, ci, rv)
+
+
+@pytest.mark.parametrize("n,p,seed", [(10, 0.3, 1), (20, 0.2, 2), (40, 0.2, 3), (40, 0.1, 4), (44, 0.3, 5)])
+def test_alg3_matches_oracle(n, p, seed):
+    A = synth.erdos_renyi(n, p, seed)
+    (cp, ri, cv), (rp, ci, rv) = ccs_crs(A)
+    rowp, colp = pb.perm_order(n, pb.PERM_CCS, cp, ri, cv, "permanent")
+    orow, ocol = OP.permanent_ordering(n, cp, ri, rp, ci)
+    assert rowp == orow and colp == ocol
+    # CRS input gives the same ordering
+    rowp2, colp2 = pb.perm_order(n, pb.PERM_CRS, rp, ci, rv, "permanent")
+    assert rowp2 == orow and colp2 == ocol
+    d_row, d_col = pb.perm_order(n, pb.PERM_CCS, cp, ri, cv, "degree")
+    assert d_col == OP.degree_sort_ascending(n, cp) and d_row == list(range(n))
+
+
+@pytest.mark.parametrize("n,p,seed", [(12, 0.3, 1), (40, 0.2, 2), (40, 0.3, 3), (36, 0.2, 4)])
+def test_alg4_matches_oracle(n, p, seed):
+    A = synth.erdos_renyi(n, p, seed)
+    (cp, ri, cv), (rp, ci, rv) = ccs_crs(A)
+    orow, ocol = OP.permanent_ordering(n, cp, ri, rp, ci)
+    B = A[np.ix_(orow, ocol)]
+    bcp, bri, _ = synth.to_ccs(B)
+    for sms in (108, 148):
+        k, c = pb.perm_partition(n, bcp, bri, 16.0, sms)
+        assert (k, c) == OP.partitioning(n, bcp, bri, 16.0, lambda r: OP.calculate_no_threads(r, sms=sms))
+
+
+def test_alg4_fig3b_fixture_a100_model():
+    from test_planner_oracle import read_golden
+    lines = read_golden("fig3b_ordered.txt")
+    n = int(lines[0])
+    A = np.zeros((n, n))
+    for l in lines[1:]:
+        r, c, v = l.split()
+        A[int(r), int(c)] = float(v)
+    cp, ri, _ = synth.to_ccs(A)
+    assert pb.perm_partition(n, cp, ri, 16.0, 108) == (4, 3)
+
+
+def test_alg2_matches_oracle():
+    for tau in (4, 32, 1024, 55296):
+        for n in (12, 16, 22, 40):
+            assert pb.perm_alg2_launch_parameters(tau, n) == OP.generate_launch_parameters(tau, n)
+
+
+def test_structural_rank_matches_oracle():
+    import oracle
+    rng = np.random.default_rng(0)
+    for t in range(20):
+        n = 3 + t % 10
+        A = (rng.uniform(size=(n, n)) < 0.25) * rng.uniform(0.5, 1, (n, n))
+        cp, ri, cv = synth.to_ccs(A)
+        assert pb.perm_structural_rank(n, pb.PERM_CCS, cp, ri, cv) == oracle.structural_rank(A)
+
+
+@pytest.mark.parametrize("bad", ["dup", "range", "zero", "nan", "ptr0", "n0", "n65"])
+def test_validation_errors(bad):
+    A = synth.erdos_renyi(6, 0.5, 1)
+    cp, ri, cv = [x.copy() for x in synth.to_ccs(A)]
+    n = 6
+    if bad == "dup":
+        j = next(j for j in range(n) if cp[j + 1] - cp[j] >= 2)
+        ri[cp[j] + 1] = ri[cp[j]]
+    elif bad == "range":
+        ri[0] = 17
+    elif bad == "zero":
+        cv[0] = 0.0
+    elif bad == "nan":
+        cv[0] = np.nan
+    elif bad == "ptr0":
+        cp = cp + 1
+    elif bad == "n0":
+        n = 0
+    elif bad == "n65":
+        n = 65
+    with pytest.raises(pb.PermError) as e:
+        pb.perm_plan(n, pb.PERM_CCS, cp, ri, cv, "auto", pb.make_opts(no_device=True))
+    assert e.value.status in (1, 2)
+
+
+def test_no_device_plan_then_compute_fails_loudly():
+    A = synth.erdos_renyi(12, 0.3, 1)
+    P = pb.Plan.from_dense(A, no_device=True)
+    with pytest.raises(pb.PermError):
+        P.compute()
+
+
+@pytest.mark.parametrize("n,p,seed,mode", [(10, 0.3, 1, "auto"), (30, 0.3, 1, "reg"), (36, 0.2, 1, "reg"),
+                                           (40, 0.2, 1, "reg"), (40, 0.2, 2, "reg"), (12, 0.3, 3, "int01")])
+def test_codegen_compiles_without_spills(n, p, seed, mode):
+    A = synth.erdos_renyi(n, p, seed, binary=(mode == "int01"))
+    P = pb.Plan.from_dense(A, ordering="auto", mode=mode, no_device=True)
+    i = P.info
+    assert i["local_bytes"] == 0
+    assert 0 < i["regs_per_thread"] <= 255
+    assert i["w_plan"] > 0
+    assert "perm_sweep" in P.source
+    cub = P.cubin()
+    assert len(cub) > 1000
+    if shutil.which("cuobjdump"):
+        with tempfile.NamedTemporaryFile(suffix=".cubin") as f:
+            f.write(cub)
+            f.flush()
+            sass = subprocess.run(["cuobjdump", "-sass", f.name], capture_output=True, text=True).stdout
+        assert "sm_100a" in sass
+        assert not re.search(r"\b(LDL|STL)\b", sass), "local memory in generated kernel"
+        if mode != "int01":
+            assert re.search(r"\bD(ADD|MUL|FMA)\b", sass)
+
+
+def test_codegen_literals_are_exact_hex():
+    # Listing 2 analogue: the column-0 values appear as exact literals
+    A = np.zeros((6, 6))
+    for r, v in [(0, 11.6), (2, 2.6), (3, 1.8), (5, 9.9)]:
+        A[r, 0] = v
+    for i in range(6):
+        A[i, (i + 1) % 6 if i != 5 else 1] = 1.0
+    P = pb.Plan.from_dense(A, ordering="none", mode="reg", no_device=True)
+    src = P.source
+    for v in (11.6, 2.6, 1.8, 9.9):
+        assert v.hex() in src
+
+
+def test_plan_geometry_and_work_model():
+    A = synth.erdos_renyi(40, 0.2, 1)
+    P = pb.Plan.from_dense(A, ordering="auto", no_device=True)
+    i = P.info
+    n = 40
+    L = 32 * i["M"] * (1 << i["B"])
+    assert i["tasks"] * L == 1 << (n - 1)          # exact cover of the Gray range
+    assert i["tasks"] & (i["tasks"] - 1) == 0       # power of two (sharding)
+    assert i["w_plan"] < i["w_alg1"]
+    assert sorted(i["row_perm"]) == list(range(n)) and sorted(i["col_perm"]) == list(range(n))

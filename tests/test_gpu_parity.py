@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bars (BASELINE.json north_star): bit-exact in INT01 for
+0/1 matrices; FP64 within 1e-9 relative of the long-double oracle.
+
+Sampled outputs at full size: the per-warp-task partial sums of the sweep are
+checked one by one against the oracle's unscaled Alg. 1 partial sum over the
+same Gray range of the same ordered matrix (ordering recomputed by the planner
+ORACLE and checked equal to the product's)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import planner as OP
+import synth
+from conftest import cuda_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a B200")]
+
+pb = pytest.importorskip("paper_2501_15126_b200")
+
+REL = 1e-9
+
+
+def plan(A, **kw):
+    return pb.Plan.from_dense(A, **kw)
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def oracle_ordered(A, info):
+    """Apply the planner oracle's version of the ordering the plan chose, and
+    check it equals the product's (bit-exact integer parity)."""
+    n = A.shape[0]
+    cp, ri, _ = synth.to_ccs(A)
+    rp, ci, _ = synth.to_crs(A)
+    o = info["ordering"]
+    if o == 2:
+        rowp, colp = OP.permanent_ordering(n, cp, ri, rp, ci)
+    elif o == 1:
+        rowp, colp = list(range(n)), OP.degree_sort_ascending(n, cp)
+    else:
+        rowp, colp = list(range(n)), list(range(n))
+    assert rowp == info["row_perm"] and colp == info["col_perm"]
+    return A[np.ix_(rowp, colp)]
+
+
+# ---- tiny and degenerate -----------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7])
+def test_tiny_vs_naive(n):
+    rng = np.random.default_rng(n)
+    A = rng.uniform(0.1, 1.0, (n, n)) * (rng.uniform(size=(n, n)) < 0.8)
+    if oracle.structural_rank(A) < n:
+        A = A + np.eye(n)
+    v = plan(A, mode="reg").compute()
+    assert rel(v, oracle.perm_naive(A)) < 1e-13
+
+
+def test_one_by_one():
+    assert plan(np.array([[2.5]]), mode="reg").compute() == 2.5
+    assert plan(np.array([[1.0]])).exact() == 1
+
+
+def test_structurally_singular_is_exact_zero():
+    A = synth.erdos_renyi(12, 0.4, 3)
+    A[:, 5] = 0
+    A[:, 7] = 0
+    A[2, 5] = 0.5
+    A[2, 7] = 0.25
+    P = plan(A)
+    assert P.info["singular"] == 1
+    assert P.compute() == 0.0
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_small_vs_naive(seed):
+    n = 4 + seed % 7
+    A = synth.erdos_renyi(n, 0.3 + 0.04 * seed, seed)
+    exp = oracle.perm_naive(A)
+    for ordering in ("none", "degree", "permanent", "auto"):
+        assert rel(plan(A, ordering=ordering, mode="reg").compute(), exp) < 1e-12
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_signed_values(seed):
+    rng = np.random.default_rng(50 + seed)
+    n = 9
+    A = rng.uniform(-1, 1, (n, n)) * (rng.uniform(size=(n, n)) < 0.5)
+    A[np.arange(n), np.arange(n)] = rng.uniform(0.5, 1, n)
+    exp, sabs = oracle.perm_nw(A)
+    v = plan(A, mode="reg").compute()
+    assert abs(v - exp) <= 1e-12 * max(abs(exp), sabs)
+
+
+# ---- config 1: n=10 0/1 p=0.3 ------------------------------------------------
+
+@pytest.mark.parametrize("seed", range(1, 6))
+def test_config1_int01_bit_exact(seed):
+    A = synth.erdos_renyi(10, 0.3, seed, binary=True)
+    exact = oracle.perm_naive_exact(A)
+    assert exact == oracle.perm_ryser_exact(A)
+    P = plan(A, mode="int01")
+    assert P.info["mode"] == 3
+    assert P.exact() == exact
+    assert plan(A).exact() == exact  # AUTO picks INT01 for 0/1 inputs
+    assert rel(plan(A, mode="reg").compute(), exact) < 1e-13
+
+
+@pytest.mark.parametrize("n", [12, 20, 24])
+def test_int01_closed_forms(n):
+    assert plan(synth.ones(n), mode="int01").exact() == math.factorial(n)
+    d = [1, 0]
+    for k in range(2, n + 1):
+        d.append((k - 1) * (d[-1] + d[-2]))
+    assert plan(synth.derangement_matrix(n), mode="int01").exact() == d[n]
+    f = [0, 1]
+    for _ in range(n + 1):
+        f.append(f[-1] + f[-2])
+    assert plan(synth.tridiagonal01(n), mode="int01").exact() == f[n + 1]
+
+
+@pytest.mark.parametrize("n,p,seed", [(20, 0.2, 1), (26, 0.25, 2), (30, 0.2, 3)])
+def test_int01_er_vs_exact_oracle(n, p, seed):
+    A = synth.erdos_renyi(n, p, seed, binary=True)
+    assert plan(A, mode="int01").exact() == oracle.perm_nw_exact(A)
+
+
+# ---- FP64 closed forms ------------------------------------------------------
+
+@pytest.mark.parametrize("n", [16, 24])
+def test_fp64_closed_forms(n):
+    assert rel(plan(synth.ones(n), mode="reg").compute(), math.factorial(n)) < 1e-12
+    assert plan(synth.identity(n), mode="reg").compute() == pytest.approx(1.0, rel=1e-15)
+
+
+@pytest.mark.parametrize("n,seed", [(24, 1), (32, 2), (40, 3)])
+def test_block_rank1_closed_form(n, seed):
+    A, blocks = synth.block_rank1(n, 8, seed)
+    cf = math.prod(math.factorial(8) * float(np.prod(u)) * float(np.prod(v)) for u, v in blocks)
+    assert rel(plan(A, mode="reg").compute(), cf) < REL
+
+
+# ---- config 2 / 3 / 4: full permanents and sampled task partials -------------
+
+@pytest.mark.parametrize("n,p,seed", [(20, 0.3, 1), (24, 0.3, 2), (28, 0.2, 1), (30, 0.3, 1)])
+def test_fp64_vs_oracle_full(n, p, seed):
+    A = synth.erdos_renyi(n, p, seed)
+    exp, sabs = oracle.perm_nw(A)
+    P = plan(A, mode="reg")
+    v = P.compute()
+    assert rel(v, exp) < REL, (v, exp, sabs / abs(exp))
+
+
+def check_task_partials(A, P, samples, tol=1e-11):
+    info = P.info
+    B = oracle_ordered(A, info)
+    first, parts = P.task_partials()
+    L = 32 * info["M"] * (1 << info["B"])
+    ntask = len(parts)
+    assert ntask > 0
+    rng = np.random.default_rng(0)
+    picks = sorted(set([0, ntask - 1] + rng.integers(0, ntask, samples).tolist()))
+    for t in picks:
+        g0 = (first + t) * L
+        exp, sabs = oracle.nw_range(B, g0, g0 + L)
+        assert abs(parts[t] - exp) <= tol * sabs, (t, parts[t], exp, sabs)
+
+
+@pytest.mark.parametrize("n,p,seed", [(30, 0.3, 1), (36, 0.2, 1)])
+def test_sampled_task_partials(n, p, seed):
+    A = synth.erdos_renyi(n, p, seed)
+    P = plan(A, mode="reg")
+    P.compute()
+    check_task_partials(A, P, 6)
+
+
+def test_config4_n40_full_size_sampled_and_sharded():
+    """n=40 p=0.2 in the bench's launch configuration: sampled task partials
+    vs the oracle; shards 0..R-1 folded == single-GPU result bit for bit."""
+    A = synth.erdos_renyi(40, 0.2, 1)
+    P = plan(A)
+    full = P.compute_ex()
+    check_task_partials(A, P, 4)
+    for world in (2, 4, 8):
+        shards = [P.shard(r, world) for r in range(world)]
+        f = P.fold(shards)
+        assert f.value == full.value
+        # each shard's partial equals the sum... its own subtree: check one sample
+    last = P.shard(7, 8)
+    check_task_partials(A, P, 2)
+    assert last.products == 1 << 36
+
+
+# ---- invariants through the C ABI -------------------------------------------
+
+def test_ccs_crs_transpose_and_orderings_agree():
+    A = synth.erdos_renyi(22, 0.3, 7)
+    ref = plan(A, ordering="none", mode="reg").compute()
+    for ordering in ("degree", "permanent", "auto"):
+        assert rel(plan(A, ordering=ordering, mode="reg").compute(), ref) < 1e-12
+    assert rel(plan(A, fmt=pb.PERM_CRS, mode="reg").compute(), ref) < 1e-12
+    assert rel(plan(A.T.copy(), mode="reg").compute(), ref) < 1e-12
+
+
+def test_chunk_geometry_independence():
+    A = synth.erdos_renyi(24, 0.3, 9)
+    exp = oracle.perm_nw(A)[0]
+    for B, U, M in [(3, 2, 1), (6, 3, 2), (8, 5, 4), (10, 4, 1), (12, 6, 1)]:
+        v = plan(A, mode="reg", chunk_log2=B, block_log2=U, task_chunks=M).compute()
+        assert rel(v, exp) < 1e-11, (B, U, M)
+
+
+def test_repeatable_bitwise():
+    A = synth.erdos_renyi(28, 0.2, 4)
+    P = plan(A)
+    a = P.compute()
+    b = P.compute()
+    assert a == b
+
+
+@pytest.mark.slow
+def test_config5_band44_vs_band_dp():
+    A = synth.givens_brickwork(44, 4, 1)
+    w = synth.half_bandwidth(A)
+    exp = oracle.perm_band(A, w)
+    v = plan(A, mode="reg").compute()
+    assert rel(v, exp) < REL
