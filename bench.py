@@ -188,7 +188,10 @@ def main():
     A, cfg = workload(args)
     n = A.shape[0]
     steps_per_perm = 2 ** (n - 1) - 1
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the plan launches on it and the step
+    # events are recorded on it
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     kw = dict(mode=args.mode, device=local, stream=stream.cuda_stream, chunk_log2=args.chunk_log2,
               block_log2=args.block_log2, task_chunks=args.task_chunks)
     ptr, idx, val = pb.dense_to_ccs(A)

@@ -278,9 +278,10 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
   g.line(std::string(g.PT()) + " cacc = 0;");
   double ops_body = 0, ops_switch = 0;
   if (U == 0) {
-    // B == 0: one product per chunk, everything frozen
+    // B == 0: one product per chunk (g = chunk), everything frozen; sign (-1)^g
     g.ops = 0;
-    g.line("cacc = " + (g.has_frozen ? std::string("F") : std::string("1")) + ";");
+    const std::string P = g.has_frozen ? std::string("F") : std::string("1");
+    g.line("cacc = (chunk & 1ull) ? (" + std::string(g.PT()) + ")(0 - " + P + ") : " + P + ";");
     ops_body = 0;
   } else {
     if (nblk > 1) {
