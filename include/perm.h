@@ -80,7 +80,10 @@ typedef struct {
   int threads_per_block; /* 0 = auto (128) */
   int no_device;         /* 1 = plan + codegen + NVRTC only; never touch a GPU
                             (for CPU-side inspection; compute calls then fail) */
-  int reserved[8];
+  int factor_cols;       /* K, closed-form summed columns (DESIGN.md "Factored
+                            columns"): 0 = auto (the K with the lowest planned
+                            work), -1 = off (plain Alg. 1 sweep), k > 0 = at most k */
+  int reserved[7];
 } perm_opts;
 
 /* Result of a computation. */
@@ -104,7 +107,13 @@ typedef struct {
   int k, c;               /* Alg. 4 partition (B200 register model) */
   int B, U;               /* chunk and unrolled-block log2 */
   int M;                  /* chunks per lane per warp-task */
-  uint64_t tasks;         /* warp-tasks over the whole Gray range (power of two) */
+  int K;                  /* factored leading columns: pairwise row-disjoint ordered
+                             columns 0..K-1 summed in closed form; the sweep runs
+                             over h-space = states of columns K..n-2 (2^(n-1-K)) */
+  uint64_t tasks;         /* warp-tasks over the whole h-range (power of two);
+                             task t covers h in [t*L, (t+1)*L), L = 32*M*2^B, i.e.
+                             Gray steps g in [t*L*2^K, (t+1)*L*2^K); its partial
+                             times (-1)^K equals the Alg. 1 partial sum there */
   int reg_rows;           /* rows of x held in registers */
   int tier_rows;          /* HYBRID rows in the per-thread tier */
   int seed_rows;          /* rows untouched by columns < B: folded into one

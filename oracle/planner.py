@@ -141,6 +141,25 @@ def permanent_ordering(n: int, cptrs, rids, rptrs, cids):
     return rowPerm, colPerm
 
 
+def factored_order(n: int, cptrs, rids, base_colp, K: int):
+    """Column order with K closed-form summed columns in front (DESIGN.md
+    "Factored columns", a B200-design extension of Sec. V's ordering): walk
+    base_colp[0..n-2] and take a column if its rows are disjoint from the rows
+    of the columns already taken, until K are taken; they go first in pick
+    order, the rest keep base order (the base's last column stays last)."""
+    picks, used = [], set()
+    for c in base_colp[: n - 1]:
+        if len(picks) == K:
+            break
+        rows = set(rids[cptrs[c]:cptrs[c + 1]])
+        if rows and not rows & used:
+            picks.append(c)
+            used |= rows
+    if len(picks) != K:
+        raise ValueError("fewer than K row-disjoint columns")
+    return picks + [c for c in base_colp if c not in picks]
+
+
 def degree_sort_ascending(n: int, cptrs):
     """Sec. VI-B: columns by nonzero count ascending, ties by index."""
     return sorted(range(n), key=lambda j: (cptrs[j + 1] - cptrs[j], j))

@@ -27,6 +27,12 @@ void order_permanent(const Csx& ccs, const Csx& crs, std::vector<int>& rowp, std
 void order_degree(const Csx& ccs, std::vector<int>& rowp, std::vector<int>& colp);
 // ordered(i, j) = a(rowp[i], colp[j]); returns CCS of the ordered matrix
 Csx permute_ccs(const Csx& ccs, const std::vector<int>& rowp, const std::vector<int>& colp);
+// Factored columns (DESIGN "Factored columns"): greedy pairwise row-disjoint
+// picks among base_colp[0..n-2] in base order, at most kmax.
+std::vector<int> factor_picks(const Csx& ccs, const std::vector<int>& base_colp, int kmax);
+// column order with the first K picks moved to the front (pick order), the
+// other columns in base order (the base's last column stays last).
+std::vector<int> factored_columns(const std::vector<int>& base_colp, const std::vector<int>& picks, int K);
 uint64_t b200_threads(int nregisters, int sms);  // CalculateNoThreads model
 void partition_alg4(const Csx& ordered_ccs, double gr_ratio, int sms, int& k, int& c);
 int alg2_launch_parameters(uint64_t tau, int n, uint64_t* out, int cap);
@@ -34,6 +40,7 @@ int alg2_launch_parameters(uint64_t tau, int n, uint64_t* out, int cap);
 // ---- codegen.cpp -----------------------------------------------------------
 struct KernelSpec {
   int n = 0;
+  int K = 0;                   // factored (pairwise row-disjoint) leading columns
   int B = 0, U = 0, M = 1;     // chunk log2, unrolled block log2, chunks per lane per task
   int mode = PERM_MODE_REG;    // REG / HYBRID / INT01
   int hybrid_c = 0;            // HYBRID: levels >= hybrid_c live in the shared tier

@@ -82,12 +82,12 @@ __global__ void fold_f64(const double* __restrict__ part, int world, double scal
 }
 
 // INT01: T' total; perm = (-1)^(n-1) T' / 2^(n-1) (exact arithmetic shift)
-__global__ void fold_u128(const u128* __restrict__ part, int world, int n, u128* __restrict__ out) {
+__global__ void fold_u128(const u128* __restrict__ part, int world, int n, int neg, u128* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   u128 T = 0;
   for (int k = 0; k < world; ++k) T += part[k];
   __int128 v = (__int128)T >> (n - 1);
-  if ((n - 1) & 1) v = -v;
+  if (((n - 1) ^ neg) & 1) v = -v;
   *out = (u128)v;
 }
 
@@ -107,10 +107,15 @@ cudaError_t libperm_launch_tree_reduce(const void* slots, uint64_t count, int is
   return cudaGetLastError();
 }
 
-cudaError_t libperm_launch_fold(const void* partials, int world, int n, int is_u128, void* out,
+// neg: extra factor (-1) (K odd: each closed-form summed column contributes -1)
+cudaError_t libperm_launch_fold(const void* partials, int world, int n, int is_u128, int neg, void* out,
                                 cudaStream_t st) {
-  if (is_u128) fold_u128<<<1, 32, 0, st>>>((const u128*)partials, world, n, (u128*)out);
-  else fold_f64<<<1, 32, 0, st>>>((const double*)partials, world, (n % 2) ? 2.0 : -2.0, (double*)out);
+  if (is_u128) {
+    fold_u128<<<1, 32, 0, st>>>((const u128*)partials, world, n, neg & 1, (u128*)out);
+  } else {
+    const double scale = ((n % 2) ? 2.0 : -2.0) * ((neg & 1) ? -1.0 : 1.0);
+    fold_f64<<<1, 32, 0, st>>>((const double*)partials, world, scale, (double*)out);
+  }
   return cudaGetLastError();
 }
 

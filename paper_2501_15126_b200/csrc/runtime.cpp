@@ -18,8 +18,8 @@
 
 extern "C" cudaError_t libperm_launch_tree_reduce(const void* slots, uint64_t count, int is_u128, void* out,
                                                   cudaStream_t st);
-extern "C" cudaError_t libperm_launch_fold(const void* partials, int world, int n, int is_u128, void* out,
-                                           cudaStream_t st);
+extern "C" cudaError_t libperm_launch_fold(const void* partials, int world, int n, int is_u128, int neg,
+                                           void* out, cudaStream_t st);
 
 using namespace perm;
 
@@ -347,26 +347,37 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
   I.mode = mode;
   p->is_u128 = mode == PERM_MODE_INT01;
 
-  // ---- geometry: B, U, M, tasks  (Lemma 1 aligned chunks; DESIGN "Chunk grid")
-  const int nb = n - 1;  // Gray bits
-  int B = p->opts.chunk_log2 > 0 ? p->opts.chunk_log2 : std::min(12, std::max(0, nb - 5));
-  if (B > nb) B = nb;
-  if (n == 1) B = 0;
-  int U = p->opts.block_log2 > 0 ? p->opts.block_log2 : 5;
-  if (U > B) U = B;
-  const uint64_t nchunks = n >= 2 ? (1ull << (nb - B)) : 1;
-  const uint64_t warp_chunks = std::max<uint64_t>(1, nchunks / 32);
-  uint64_t M = p->opts.task_chunks > 0 ? (uint64_t)p->opts.task_chunks : 0;
-  if (M == 0) {
-    M = 1;
-    while (warp_chunks / (M * 2) >= (1ull << 16)) M *= 2;
+  // ---- geometry for a sweep over nb h-bits: B, U, M, tasks (Lemma 1 aligned
+  // chunks; DESIGN "Chunk grid").  Depends only on (n, K, opts): identical on
+  // every rank, so shards are complete subtrees of the same reduction tree.
+  if (p->opts.task_chunks > 0 && (p->opts.task_chunks & (p->opts.task_chunks - 1))) {
+    delete p;
+    return fail(PERM_EINVAL, "task_chunks must be a power of two");
   }
-  if (M & (M - 1)) { delete p; return fail(PERM_EINVAL, "task_chunks must be a power of two"); }
-  if (M > warp_chunks) M = warp_chunks;
-  I.B = B;
-  I.U = U;
-  I.M = (int)M;
-  I.tasks = warp_chunks / M;
+  auto geometry = [&](int K, KernelSpec& sp) {
+    const int nb = std::max(0, n - 1 - K);  // h-bits
+    int B = p->opts.chunk_log2 > 0 ? p->opts.chunk_log2 : std::min(12, std::max(0, nb - 5));
+    if (B > nb) B = nb;
+    int U = p->opts.block_log2 > 0 ? p->opts.block_log2 : 5;
+    if (U > B) U = B;
+    const uint64_t nchunks = 1ull << (nb - B);
+    const uint64_t warp_chunks = std::max<uint64_t>(1, nchunks / 32);
+    uint64_t M = p->opts.task_chunks > 0 ? (uint64_t)p->opts.task_chunks : 0;
+    if (M == 0) {
+      M = 1;
+      while (warp_chunks / (M * 2) >= (1ull << 16)) M *= 2;
+    }
+    if (M > warp_chunks) M = warp_chunks;
+    sp.n = n;
+    sp.K = K;
+    sp.B = B;
+    sp.U = U;
+    sp.M = (int)M;
+    sp.mode = mode;
+    sp.threads = p->opts.threads_per_block > 0 ? p->opts.threads_per_block : 128;
+    sp.nchunks_total = nchunks;
+    return warp_chunks / M;  // tasks
+  };
 
   // ---- ordering
   auto order_with = [&](int o, std::vector<int>& rp, std::vector<int>& cp) {
@@ -375,13 +386,6 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     else { rp.resize(n); cp.resize(n); for (int i = 0; i < n; ++i) rp[i] = cp[i] = i; }
   };
   if (ord < PERM_ORDER_NONE || ord > PERM_ORDER_AUTO) { delete p; return fail(PERM_EINVAL, "unknown ordering"); }
-  p->spec.n = n;
-  p->spec.B = B;
-  p->spec.U = U;
-  p->spec.M = (int)M;
-  p->spec.mode = mode;
-  p->spec.threads = p->opts.threads_per_block > 0 ? p->opts.threads_per_block : 128;
-  p->spec.nchunks_total = nchunks;
   auto make_x0 = [&](const Csx& o) {  // Alg. 1 lines 1-5 (reading R1: true a_{i,n-1})
     Csx orr = transpose(o);
     std::vector<double> x0(n);
@@ -398,22 +402,47 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
   std::vector<double> x0;
   {
     const double tc = now_ms();
-    int chosen = ord;
-    if (ord == PERM_ORDER_AUTO) {
-      double best = 1e300;
-      for (int cand : {PERM_ORDER_PERMANENT, PERM_ORDER_DEGREE, PERM_ORDER_NONE}) {
-        std::vector<int> rp, cp;
-        order_with(cand, rp, cp);
-        Csx o = permute_ccs(p->ccs, rp, cp);
-        KernelCode kc = generate_kernel(o, make_x0(o), p->spec);
-        if (kc.w_plan < best - 1e-12) { best = kc.w_plan; chosen = cand; }
+    // candidates: base ordering x K factored columns (greedy row-disjoint
+    // picks in base order, DESIGN "Factored columns"); pick the lowest W_plan
+    int kcap = p->opts.factor_cols < 0 ? 0 : (p->opts.factor_cols > 0 ? p->opts.factor_cols : 16);
+    if (p->singular || n < 3) kcap = 0;
+    std::vector<int> bases;
+    if (ord == PERM_ORDER_AUTO) bases = {PERM_ORDER_PERMANENT, PERM_ORDER_DEGREE};
+    else bases = {(int)ord};
+    double best = 1e300;
+    int best_base = bases[0], best_K = 0;
+    for (int base : bases) {
+      std::vector<int> rp, cp;
+      order_with(base, rp, cp);
+      std::vector<int> picks = factor_picks(p->ccs, cp, kcap);
+      const int kmax = (int)picks.size();
+      for (int K = (p->opts.factor_cols > 0 ? kmax : 0); K <= kmax; ++K) {
+        if (bases.size() == 1 && kmax == 0) break;  // nothing to compare
+        std::vector<int> cpk = factored_columns(cp, picks, K);
+        Csx o = permute_ccs(p->ccs, rp, cpk);
+        KernelSpec sp;
+        geometry(K, sp);
+        KernelCode kc = generate_kernel(o, make_x0(o), sp);
+        if (kc.w_plan < best * (1 - 1e-9)) { best = kc.w_plan; best_base = base; best_K = K; }
       }
     }
-    order_with(chosen, p->rowp, p->colp);
+    std::vector<int> rp, cp;
+    order_with(best_base, rp, cp);
+    std::vector<int> picks = factor_picks(p->ccs, cp, kcap);
+    p->rowp = rp;
+    p->colp = factored_columns(cp, picks, best_K);
     p->occs = permute_ccs(p->ccs, p->rowp, p->colp);
-    I.ordering = chosen;
+    I.ordering = best_base;
+    I.tasks = geometry(best_K, p->spec);
+    I.K = best_K;
+    I.B = p->spec.B;
+    I.U = p->spec.U;
+    I.M = p->spec.M;
     for (int i = 0; i < n; ++i) { I.row_perm[i] = p->rowp[i]; I.col_perm[i] = p->colp[i]; }
-    partition_alg4(p->occs, gr, 148, I.k, I.c);
+    {  // Alg. 4 partition reported for the base ordering (paper's (k, c))
+      Csx ob = permute_ccs(p->ccs, rp, cp);
+      partition_alg4(ob, gr, 148, I.k, I.c);
+    }
     x0 = make_x0(p->occs);
     if (n == 1) {
       p->trivial1 = true;
@@ -524,7 +553,7 @@ int perm_compute_shard(perm_plan_t p, int rank, int world, perm_result* r) {
   fill_result(p, r, raw, false);
   r->world = world;
   r->rank = rank;
-  r->products = count * 32ull * (uint64_t)p->info.M << p->info.B;
+  r->products = (count * 32ull * (uint64_t)p->info.M << p->info.B) << p->info.K;
   r->sweep_ms = sm;
   r->reduce_ms = rm;
   return PERM_OK;
@@ -535,7 +564,7 @@ int perm_fold_async(perm_plan_t p, const void* d_partials, int world, void* d_ou
   if (world < 1 || world > 128 || (world & (world - 1))) return fail(PERM_EINVAL, "world must be a power of two <= 128");
   CUDA_TRY(cudaSetDevice(p->device));
   const int nn = p->trivial1 ? 1 : p->n;
-  CUDA_TRY(libperm_launch_fold(d_partials, world, nn, p->is_u128, d_out, p->stream));
+  CUDA_TRY(libperm_launch_fold(d_partials, world, nn, p->is_u128, p->info.K & 1, d_out, p->stream));
   return PERM_OK;
 }
 

@@ -168,12 +168,36 @@ def test_codegen_literals_are_exact_hex():
         assert v.hex() in src
 
 
+@pytest.mark.parametrize("n,p,seed", [(12, 0.3, 1), (30, 0.3, 1), (36, 0.2, 1), (40, 0.2, 1), (40, 0.2, 2)])
+@pytest.mark.parametrize("fc", [0, 2, -1])
+def test_factored_ordering_matches_oracle(n, p, seed, fc):
+    A = synth.erdos_renyi(n, p, seed)
+    P = pb.Plan.from_dense(A, ordering="auto", mode="reg", factor_cols=fc, no_device=True)
+    i = P.info
+    cp, ri, _ = synth.to_ccs(A)
+    rp, ci, _ = synth.to_crs(A)
+    if i["ordering"] == 2:
+        rowp, colp = OP.permanent_ordering(n, cp, ri, rp, ci)
+    else:
+        rowp, colp = list(range(n)), OP.degree_sort_ascending(n, cp)
+    assert i["row_perm"] == rowp
+    assert i["col_perm"] == OP.factored_order(n, cp, ri, colp, i["K"])
+    if fc == -1:
+        assert i["K"] == 0
+    if fc > 0:
+        assert i["K"] <= fc
+    # factored columns are pairwise row-disjoint
+    B = A[np.ix_(i["row_perm"], i["col_perm"])]
+    if i["K"]:
+        assert np.all((B[:, :i["K"]] != 0).sum(axis=1) <= 1)
+
+
 def test_plan_geometry_and_work_model():
     A = synth.erdos_renyi(40, 0.2, 1)
     P = pb.Plan.from_dense(A, ordering="auto", no_device=True)
     i = P.info
     n = 40
-    L = 32 * i["M"] * (1 << i["B"])
+    L = 32 * i["M"] * (1 << i["B"]) << i["K"]
     assert i["tasks"] * L == 1 << (n - 1)          # exact cover of the Gray range
     assert i["tasks"] & (i["tasks"] - 1) == 0       # power of two (sharding)
     assert i["w_plan"] < i["w_alg1"]
