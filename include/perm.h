@@ -83,7 +83,9 @@ typedef struct {
   int factor_cols;       /* K, closed-form summed columns (DESIGN.md "Factored
                             columns"): 0 = auto (the K with the lowest planned
                             work), -1 = off (plain Alg. 1 sweep), k > 0 = at most k */
-  int reserved[7];
+  int min_blocks;        /* __launch_bounds__ min blocks per SM (register cap);
+                            0 = auto from the planner's register estimate */
+  int reserved[6];
 } perm_opts;
 
 /* Result of a computation. */

@@ -273,11 +273,24 @@ struct Gen {
       ops += 1;  // e - Q0
       std::string d = "(" + e + " - " + qexpr(0) + ")";
       std::string t = "t" + std::to_string(tmp++);
-      line(std::string("const ") + PT() + " " + t + " = " + mul(d, above(0)) + ";");
-      // pairwise (binary-counter) accumulation of the pair terms
-      std::string v = t;
+      std::string v;
       int lvl = 0;
       unsigned kk = (unsigned)k;
+      const std::string ab = above(0);
+      if ((kk & 1u) && !ab.empty() && !i01) {
+        // first merge of the pairwise tree fused with the pair product:
+        // t = fma(d, S_above, stack[0]) -- one DFMA (the kernel is compiled
+        // with --fmad=false, so every emitted op is exactly one instruction)
+        ops += 1;
+        line(std::string("const ") + PT() + " " + t + " = fma(" + d + ", " + ab + ", " + stack[0] + ");");
+        v = t;
+        kk >>= 1;
+        ++lvl;
+      } else {
+        line(std::string("const ") + PT() + " " + t + " = " + mul(d, ab) + ";");
+        v = t;
+      }
+      // pairwise (binary-counter) accumulation of the pair terms
       while (kk & 1u) {
         std::string w = "v" + std::to_string(tmp++);
         ops += 1;

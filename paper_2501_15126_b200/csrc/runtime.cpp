@@ -58,8 +58,10 @@ int nvrtc_compile(const std::string& src, std::vector<char>& cubin, std::string&
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, src.c_str(), "perm_sweep.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
     return fail(PERM_ENVRTC, "nvrtcCreateProgram failed");
+  // --fmad=false: every arithmetic op the generator emits (and counts in
+  // W_plan) is exactly one DADD/DMUL/DFMA; fusions are emitted explicitly.
   std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
-                                   "--ptxas-options=-v", "-default-device"};
+                                   "--ptxas-options=-v", "-default-device", "--fmad=false"};
   if (int128) opts.push_back("--device-int128");
   nvrtcResult r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
   size_t ls = 0;
@@ -354,9 +356,9 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     delete p;
     return fail(PERM_EINVAL, "task_chunks must be a power of two");
   }
-  auto geometry = [&](int K, KernelSpec& sp) {
+  auto geometry = [&](int K, KernelSpec& sp, int bcap) {
     const int nb = std::max(0, n - 1 - K);  // h-bits
-    int B = p->opts.chunk_log2 > 0 ? p->opts.chunk_log2 : std::min(12, std::max(0, nb - 5));
+    int B = p->opts.chunk_log2 > 0 ? p->opts.chunk_log2 : std::min(bcap, std::max(0, nb - 5));
     if (B > nb) B = nb;
     int U = p->opts.block_log2 > 0 ? p->opts.block_log2 : 5;
     if (U > B) U = B;
@@ -409,52 +411,111 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     std::vector<int> bases;
     if (ord == PERM_ORDER_AUTO) bases = {PERM_ORDER_PERMANENT, PERM_ORDER_DEGREE};
     else bases = {(int)ord};
-    double best = 1e300;
-    int best_base = bases[0], best_K = 0;
+    std::vector<int> bcaps = {12, 10, 8};
+    if (p->opts.chunk_log2 > 0) bcaps = {p->opts.chunk_log2};
+    // FP64-pipe efficiency vs resident 128-thread blocks per SM (1 warp per
+    // SMSP each); calibrated on B200.
+    auto eff = [](int bps) { return bps >= 4 ? 1.0 : bps == 3 ? 0.95 : bps == 2 ? 0.8 : 0.5; };
+    auto bps_of = [&](int regs, int threads) {
+      const int r8 = (std::max(regs, 16) + 7) / 8 * 8;
+      return std::max(1, std::min(16, 65536 / (threads * r8)));
+    };
+    struct Cand { double score, w; int base, K, bcap, est; };
+    std::vector<Cand> cands;
     for (int base : bases) {
       std::vector<int> rp, cp;
       order_with(base, rp, cp);
       std::vector<int> picks = factor_picks(p->ccs, cp, kcap);
       const int kmax = (int)picks.size();
       for (int K = (p->opts.factor_cols > 0 ? kmax : 0); K <= kmax; ++K) {
-        if (bases.size() == 1 && kmax == 0) break;  // nothing to compare
         std::vector<int> cpk = factored_columns(cp, picks, K);
         Csx o = permute_ccs(p->ccs, rp, cpk);
-        KernelSpec sp;
-        geometry(K, sp);
-        KernelCode kc = generate_kernel(o, make_x0(o), sp);
-        if (kc.w_plan < best * (1 - 1e-9)) { best = kc.w_plan; best_base = base; best_K = K; }
+        std::vector<double> xo = make_x0(o);
+        for (int bc : bcaps) {
+          KernelSpec sp;
+          geometry(K, sp, bc);
+          if (bc != bcaps[0] && sp.B != bc) continue;  // cap not binding: duplicate
+          KernelCode kc = generate_kernel(o, xo, sp);
+          const double score = kc.w_plan / eff(bps_of(kc.est_regs, sp.threads));
+          cands.push_back({score, kc.w_plan, base, K, bc, kc.est_regs});
+        }
       }
     }
-    std::vector<int> rp, cp;
-    order_with(best_base, rp, cp);
-    std::vector<int> picks = factor_picks(p->ccs, cp, kcap);
-    p->rowp = rp;
-    p->colp = factored_columns(cp, picks, best_K);
-    p->occs = permute_ccs(p->ccs, p->rowp, p->colp);
-    I.ordering = best_base;
-    I.tasks = geometry(best_K, p->spec);
-    I.K = best_K;
+    std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.score < b.score; });
+    if (cands.size() > 3) cands.resize(3);
+    if (p->singular || n == 1) cands.resize(std::min<size_t>(cands.size(), 1));
+    // compile the top candidates (NVRTC, spill gate with escalation) and keep
+    // the best by W_plan / eff(actual registers)
+    double best_score = 1e300;
+    bool have = false;
+    for (const Cand& c : cands) {
+      std::vector<int> rp, cp;
+      order_with(c.base, rp, cp);
+      std::vector<int> picks = factor_picks(p->ccs, cp, kcap);
+      std::vector<int> colp = factored_columns(cp, picks, c.K);
+      Csx o = permute_ccs(p->ccs, rp, colp);
+      std::vector<double> xo = make_x0(o);
+      KernelSpec sp;
+      uint64_t tasks = geometry(c.K, sp, c.bcap);
+      if (n == 1 || p->singular) {
+        p->rowp = rp; p->colp = colp; p->occs = o; p->spec = sp; x0 = xo;
+        I.ordering = c.base; I.tasks = tasks; I.K = c.K;
+        have = true;
+        break;
+      }
+      KernelCode kc;
+      std::vector<char> cubin;
+      std::string log;
+      int regs = -1, stack = 0, spill = 0;
+      sp.min_blocks = p->opts.min_blocks > 0 ? p->opts.min_blocks
+                                             : bps_of(generate_kernel(o, xo, sp).est_regs + 16, sp.threads);
+      for (int attempt = 0; attempt < 24; ++attempt) {
+        kc = generate_kernel(o, xo, sp);
+        bool cached = false;
+        double ms = 0;
+        st = nvrtc_compile(kc.source, cubin, log, p->is_u128, cached, ms);
+        if (st != PERM_OK) return bail(st);
+        I.nvrtc_ms += ms;
+        I.cubin_cached = cached;
+        parse_ptxas(log, regs, stack, spill);
+        if (stack <= 0 && spill <= 0) break;
+        // escalate: larger register cap, then a shorter unrolled block, then fewer chunk bits
+        if (sp.min_blocks > 1) sp.min_blocks -= 1;
+        else if (sp.U > 2) sp.U -= 1;
+        else if (sp.B > 2 && p->opts.chunk_log2 == 0) {
+          const int keepU = sp.U;  // geometry() keeps min_blocks
+          tasks = geometry(c.K, sp, sp.B - 2);
+          sp.U = std::min(keepU, sp.B);
+        } else break;
+      }
+      if (stack > 0 || spill > 0) continue;
+      const double score = kc.w_plan / eff(bps_of(regs, sp.threads));
+      if (!have || score < best_score) {
+        have = true;
+        best_score = score;
+        p->rowp = rp; p->colp = colp; p->occs = o; p->spec = sp; x0 = xo;
+        p->code = kc; p->cubin = cubin; p->ptxas_log = log;
+        I.ordering = c.base; I.tasks = tasks; I.K = c.K;
+        I.regs_per_thread = regs;
+        I.local_bytes = 0;
+      }
+    }
+    if (!have) {
+      g_err = "every candidate kernel spills to local memory; reduce chunk_log2 or n";
+      return bail(PERM_ESPILL);
+    }
     I.B = p->spec.B;
     I.U = p->spec.U;
     I.M = p->spec.M;
     for (int i = 0; i < n; ++i) { I.row_perm[i] = p->rowp[i]; I.col_perm[i] = p->colp[i]; }
     {  // Alg. 4 partition reported for the base ordering (paper's (k, c))
+      std::vector<int> rp, cp;
+      order_with(I.ordering, rp, cp);
       Csx ob = permute_ccs(p->ccs, rp, cp);
       partition_alg4(ob, gr, 148, I.k, I.c);
     }
-    x0 = make_x0(p->occs);
-    if (n == 1) {
-      p->trivial1 = true;
-    } else if (!p->singular) {
-      // register budget -> __launch_bounds__ min blocks (65536 regs / threads)
-      KernelCode probe = generate_kernel(p->occs, x0, p->spec);
-      int cap_regs = std::max(64, ((probe.est_regs + 7) / 8) * 8 + 16);
-      int minb = std::max(1, std::min(16, 65536 / (p->spec.threads * std::min(255, cap_regs))));
-      p->spec.min_blocks = minb;
-      p->code = generate_kernel(p->occs, x0, p->spec);
-    }
-    I.codegen_ms = now_ms() - tc;
+    if (n == 1) p->trivial1 = true;
+    I.codegen_ms = now_ms() - tc - I.nvrtc_ms;
   }
   I.w_alg1 = w_alg1(p->occs);
   if (!p->singular && !p->trivial1) {
@@ -464,28 +525,6 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     I.seed_rows = p->code.seed_rows;
     I.levels = p->code.levels;
     I.block = p->spec.threads;
-    // NVRTC; retry with a larger register cap on spills
-    for (int attempt = 0; attempt < 6; ++attempt) {
-      bool cached = false;
-      double ms = 0;
-      st = nvrtc_compile(p->code.source, p->cubin, p->ptxas_log, p->is_u128, cached, ms);
-      if (st != PERM_OK) return bail(st);
-      I.nvrtc_ms += ms;
-      I.cubin_cached = cached;
-      int regs, stack, spill;
-      parse_ptxas(p->ptxas_log, regs, stack, spill);
-      I.regs_per_thread = regs;
-      I.local_bytes = std::max(stack, spill);
-      if (stack <= 0 && spill <= 0) break;
-      if (p->spec.min_blocks <= 1) break;
-      p->spec.min_blocks -= 1;
-      p->code = generate_kernel(p->occs, x0, p->spec);
-    }
-    if (I.local_bytes > 0) {
-      g_err = "generated kernel uses local memory (" + std::to_string(I.local_bytes) +
-              " bytes); reduce chunk_log2 or use HYBRID mode";
-      return bail(PERM_ESPILL);
-    }
   }
   I.plan_ms = now_ms() - t0;
   if (!p->opts.no_device) {

@@ -136,6 +136,24 @@ def block_rank1(n: int, b: int, seed: int):
     return D[np.ix_(P, Q)], blocks
 
 
+def block_diagonal(n: int, b: int, seed: int):
+    """Block-diagonal matrix of dense b x b blocks with U(0,1] entries, then
+    random row and column permutations (closed-form pin: perm = product of the
+    block permanents; density b/n).  Returns (A, [block matrices])."""
+    if n % b:
+        raise ValueError("b must divide n")
+    rng = SplitMix64(seed ^ 0xB10C)
+    D = np.zeros((n, n))
+    blocks = []
+    for k in range(n // b):
+        blk = np.array([[rng.unit_open0() for _ in range(b)] for _ in range(b)])
+        D[k * b:(k + 1) * b, k * b:(k + 1) * b] = blk
+        blocks.append(blk)
+    P = rng.permutation(n)
+    Q = rng.permutation(n)
+    return D[np.ix_(P, Q)], blocks
+
+
 def ones(n):
     return np.ones((n, n))
 

@@ -21,15 +21,18 @@ def main():
     ap.add_argument("--ks", default="-1,2,4,6")
     ap.add_argument("--bs", default="8,10,12")
     ap.add_argument("--threads", default="128")
+    ap.add_argument("--minb", default="0")
     ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
     for seed in [int(s) for s in a.seeds.split(",")]:
         A = synth.erdos_renyi(a.n, a.p, seed) if a.p > 0 else synth.givens_brickwork(a.n, 4, seed)
         for k in [int(s) for s in a.ks.split(",")]:
             for b in [int(s) for s in a.bs.split(",")]:
-                for th in [int(s) for s in a.threads.split(",")]:
+              for th in [int(s) for s in a.threads.split(",")]:
+                for mb in [int(s) for s in a.minb.split(",")]:
                     try:
-                        P = pb.Plan.from_dense(A, mode="reg", factor_cols=k, chunk_log2=b, threads_per_block=th)
+                        P = pb.Plan.from_dense(A, mode="reg", factor_cols=k, chunk_log2=b, threads_per_block=th,
+                                               min_blocks=mb)
                     except pb.PermError as e:
                         print(json.dumps({"seed": seed, "K": k, "B": b, "err": str(e)[:120]}), flush=True)
                         continue
