@@ -112,6 +112,7 @@ typedef struct {
   int K;                  /* factored leading columns: pairwise row-disjoint ordered
                              columns 0..K-1 summed in closed form; the sweep runs
                              over h-space = states of columns K..n-2 (2^(n-1-K)) */
+  int swept_order;        /* 0: swept columns in base order; 1: sorted by flip cost */
   uint64_t tasks;         /* warp-tasks over the whole h-range (power of two);
                              task t covers h in [t*L, (t+1)*L), L = 32*M*2^B, i.e.
                              Gray steps g in [t*L*2^K, (t+1)*L*2^K); its partial

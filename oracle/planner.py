@@ -160,6 +160,31 @@ def factored_order(n: int, cptrs, rids, base_colp, K: int):
     return picks + [c for c in base_colp if c not in picks]
 
 
+def costsort_swept(n: int, cptrs, rids, colp, K: int):
+    """Swept columns (positions K..n-2) stably sorted by the flip cost
+    nnz(c) + sum over touched factored groups g of dcost(|g|), dcost = 0, 2,
+    3|g|-1 for |g| = 1, 2, >= 3 (restates the product heuristic)."""
+    grp = {}
+    size = []
+    for k in range(K):
+        c = colp[k]
+        rows = rids[cptrs[c]:cptrs[c + 1]]
+        for r in rows:
+            grp[r] = k
+        size.append(len(rows))
+
+    def dcost(s):
+        return 0 if s <= 1 else (2 if s == 2 else 3 * s - 1)
+
+    def cost(c):
+        rows = rids[cptrs[c]:cptrs[c + 1]]
+        gs = {grp[r] for r in rows if r in grp}
+        return len(rows) + sum(dcost(size[g]) for g in gs)
+
+    swept = sorted(colp[K:n - 1], key=cost)   # sorted() is stable
+    return list(colp[:K]) + swept + list(colp[n - 1:])
+
+
 def degree_sort_ascending(n: int, cptrs):
     """Sec. VI-B: columns by nonzero count ascending, ties by index."""
     return sorted(range(n), key=lambda j: (cptrs[j + 1] - cptrs[j], j))

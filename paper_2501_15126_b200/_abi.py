@@ -42,7 +42,7 @@ class perm_plan_info(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int), ("nnz", ctypes.c_int), ("mode", ctypes.c_int), ("ordering", ctypes.c_int),
                 ("singular", ctypes.c_int), ("struct_rank", ctypes.c_int), ("k", ctypes.c_int),
                 ("c", ctypes.c_int), ("B", ctypes.c_int), ("U", ctypes.c_int), ("M", ctypes.c_int),
-                ("K", ctypes.c_int), ("tasks", ctypes.c_uint64), ("reg_rows", ctypes.c_int), ("tier_rows", ctypes.c_int),
+                ("K", ctypes.c_int), ("swept_order", ctypes.c_int), ("tasks", ctypes.c_uint64), ("reg_rows", ctypes.c_int), ("tier_rows", ctypes.c_int),
                 ("seed_rows", ctypes.c_int), ("levels", ctypes.c_int), ("w_plan", ctypes.c_double),
                 ("w_alg1", ctypes.c_double), ("block", ctypes.c_int), ("grid", ctypes.c_int),
                 ("blocks_per_sm", ctypes.c_int), ("sms", ctypes.c_int), ("regs_per_thread", ctypes.c_int),

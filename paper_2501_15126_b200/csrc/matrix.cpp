@@ -189,6 +189,30 @@ std::vector<int> factored_columns(const std::vector<int>& base_colp, const std::
   return out;
 }
 
+std::vector<int> costsort_swept(const Csx& ccs, const std::vector<int>& colp, int K) {
+  const int n = ccs.n;
+  std::vector<int> grp(n, -1), gsize(K, 0);
+  for (int k = 0; k < K; ++k)
+    for (int p = ccs.ptr[colp[k]]; p < ccs.ptr[colp[k] + 1]; ++p) { grp[ccs.idx[p]] = k; gsize[k]++; }
+  auto dcost = [](int k) { return k <= 1 ? 0 : (k == 2 ? 2 : 3 * k - 1); };
+  auto cost = [&](int c) {
+    int w = ccs.ptr[c + 1] - ccs.ptr[c];
+    std::vector<char> seen(K, 0);
+    for (int p = ccs.ptr[c]; p < ccs.ptr[c + 1]; ++p) {
+      int g = grp[ccs.idx[p]];
+      if (g >= 0 && !seen[g]) { seen[g] = 1; w += dcost(gsize[g]); }
+    }
+    return w;
+  };
+  std::vector<int> out(colp.begin(), colp.end());
+  if (n - 1 > K) {
+    std::vector<int> cst(n);
+    for (int q = K; q < n - 1; ++q) cst[colp[q]] = cost(colp[q]);
+    std::stable_sort(out.begin() + K, out.end() - 1, [&](int a, int b) { return cst[a] < cst[b]; });
+  }
+  return out;
+}
+
 // CalculateNoThreads (Alg. 4 line 12; undefined in the paper): resident
 // threads when each thread needs nregisters + 32 registers, on `sms` SMs of
 // 65536 registers / 2048 threads, 255 registers per thread max.

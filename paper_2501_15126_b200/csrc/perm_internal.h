@@ -33,6 +33,9 @@ std::vector<int> factor_picks(const Csx& ccs, const std::vector<int>& base_colp,
 // column order with the first K picks moved to the front (pick order), the
 // other columns in base order (the base's last column stays last).
 std::vector<int> factored_columns(const std::vector<int>& base_colp, const std::vector<int>& picks, int K);
+// swept columns (positions K..n-2) stably sorted by flip cost
+// nnz(c) + sum over touched factored groups g of dcost(|g|) (0, 2, 3|g|-1)
+std::vector<int> costsort_swept(const Csx& ccs, const std::vector<int>& colp, int K);
 uint64_t b200_threads(int nregisters, int sms);  // CalculateNoThreads model
 void partition_alg4(const Csx& ordered_ccs, double gr_ratio, int sms, int& k, int& c);
 int alg2_launch_parameters(uint64_t tau, int n, uint64_t* out, int cap);

@@ -420,26 +420,32 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
       const int r8 = (std::max(regs, 16) + 7) / 8 * 8;
       return std::max(1, std::min(16, 65536 / (threads * r8)));
     };
-    struct Cand { double score, w; int base, K, bcap, est; };
+    struct Cand { double score, w; int base, K, var, bcap, est; };
     std::vector<Cand> cands;
+    // swept-column variants: 0 = base order, 1 = sorted by flip cost (AUTO only)
+    const int nvar = ord == PERM_ORDER_AUTO ? 2 : 1;
+    auto colp_of = [&](const std::vector<int>& cp, const std::vector<int>& picks, int K, int var) {
+      std::vector<int> c = factored_columns(cp, picks, K);
+      return var ? costsort_swept(p->ccs, c, K) : c;
+    };
     for (int base : bases) {
       std::vector<int> rp, cp;
       order_with(base, rp, cp);
       std::vector<int> picks = factor_picks(p->ccs, cp, kcap);
       const int kmax = (int)picks.size();
-      for (int K = (p->opts.factor_cols > 0 ? kmax : 0); K <= kmax; ++K) {
-        std::vector<int> cpk = factored_columns(cp, picks, K);
-        Csx o = permute_ccs(p->ccs, rp, cpk);
-        std::vector<double> xo = make_x0(o);
-        for (int bc : bcaps) {
-          KernelSpec sp;
-          geometry(K, sp, bc);
-          if (bc != bcaps[0] && sp.B != bc) continue;  // cap not binding: duplicate
-          KernelCode kc = generate_kernel(o, xo, sp);
-          const double score = kc.w_plan / eff(bps_of(kc.est_regs, sp.threads));
-          cands.push_back({score, kc.w_plan, base, K, bc, kc.est_regs});
+      for (int K = (p->opts.factor_cols > 0 ? kmax : 0); K <= kmax; ++K)
+        for (int var = 0; var < nvar; ++var) {
+          Csx o = permute_ccs(p->ccs, rp, colp_of(cp, picks, K, var));
+          std::vector<double> xo = make_x0(o);
+          for (int bc : bcaps) {
+            KernelSpec sp;
+            geometry(K, sp, bc);
+            if (bc != bcaps[0] && sp.B != bc) continue;  // cap not binding: duplicate
+            KernelCode kc = generate_kernel(o, xo, sp);
+            const double score = kc.w_plan / eff(bps_of(kc.est_regs, sp.threads));
+            cands.push_back({score, kc.w_plan, base, K, var, bc, kc.est_regs});
+          }
         }
-      }
     }
     std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.score < b.score; });
     if (cands.size() > 3) cands.resize(3);
@@ -452,14 +458,14 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
       std::vector<int> rp, cp;
       order_with(c.base, rp, cp);
       std::vector<int> picks = factor_picks(p->ccs, cp, kcap);
-      std::vector<int> colp = factored_columns(cp, picks, c.K);
+      std::vector<int> colp = colp_of(cp, picks, c.K, c.var);
       Csx o = permute_ccs(p->ccs, rp, colp);
       std::vector<double> xo = make_x0(o);
       KernelSpec sp;
       uint64_t tasks = geometry(c.K, sp, c.bcap);
       if (n == 1 || p->singular) {
         p->rowp = rp; p->colp = colp; p->occs = o; p->spec = sp; x0 = xo;
-        I.ordering = c.base; I.tasks = tasks; I.K = c.K;
+        I.ordering = c.base; I.tasks = tasks; I.K = c.K; I.swept_order = c.var;
         have = true;
         break;
       }
@@ -495,7 +501,7 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
         best_score = score;
         p->rowp = rp; p->colp = colp; p->occs = o; p->spec = sp; x0 = xo;
         p->code = kc; p->cubin = cubin; p->ptxas_log = log;
-        I.ordering = c.base; I.tasks = tasks; I.K = c.K;
+        I.ordering = c.base; I.tasks = tasks; I.K = c.K; I.swept_order = c.var;
         I.regs_per_thread = regs;
         I.local_bytes = 0;
       }

@@ -45,6 +45,8 @@ def oracle_ordered(A, info):
     else:
         rowp, colp = list(range(n)), list(range(n))
     colp = OP.factored_order(n, cp, ri, colp, info["K"])
+    if info["swept_order"] == 1:
+        colp = OP.costsort_swept(n, cp, ri, colp, info["K"])
     assert rowp == info["row_perm"] and colp == info["col_perm"]
     return A[np.ix_(rowp, colp)]
 
