@@ -274,7 +274,9 @@ def main():
     if rank == 0:
         clocks = clk.summary()
         sw = sum(sweep_ms) / len(sweep_ms)
-        products = (info["tasks"] // world if info["tasks"] >= world else 1) * 32 * info["M"] * (1 << info["B"])
+        # Gray steps one sweep launch covers (h-steps x 2^K)
+        products = ((info["tasks"] // world if info["tasks"] >= world else 1) * 32 * info["M"]
+                    * (1 << info["B"]) << info["K"])
         achieved = info["w_plan"] * products / (sw / 1000.0) / 1e12
         sm_max = clocks.get("sm_max_mhz") or 1965.0
         peak = info["sms"] * 64 * sm_max * 1e6 / 1e12

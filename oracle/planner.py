@@ -179,7 +179,8 @@ def costsort_swept(n: int, cptrs, rids, colp, K: int):
     def cost(c):
         rows = rids[cptrs[c]:cptrs[c + 1]]
         gs = {grp[r] for r in rows if r in grp}
-        return len(rows) + sum(dcost(size[g]) for g in gs)
+        live = sum(1 for r in rows if r not in grp or size[grp[r]] > 1)   # single-row groups: dead rows
+        return live + sum(dcost(size[g]) for g in gs)
 
     swept = sorted(colp[K:n - 1], key=cost)   # sorted() is stable
     return list(colp[:K]) + swept + list(colp[n - 1:])

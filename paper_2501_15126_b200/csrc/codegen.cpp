@@ -213,8 +213,13 @@ struct Gen {
     line("S" + std::to_string(l) + " = " + mul(qexpr(l), above(l)) + ";");
   }
 
+  // a row of a single-row factored column only enters through D_k = a_rk:
+  // its y value is never needed (no register, no updates)
+  bool dead_row(int r) const { return fac[fac_of_row[r]].constant(); }
+
   // one update y_r +-= a_rj.  sign: "+", "-" (static) or a runtime +-1 name
   void update(int r, double a, const std::string& sign) {
+    if (dead_row(r)) return;
     ops += 1;
     if (i01) {
       if (sign == "+") line(xv(r) + " += 2;");
@@ -310,20 +315,28 @@ struct Gen {
     const int nbits = n - 1 - K;
     line("const u64 gr = h0 ^ (h0 >> 1);");
     for (int r = 0; r < n; ++r) {
+      if (dead_row(r)) continue;
       if (i01) line(std::string(VT()) + " " + xv(r) + " = " + std::to_string((long long)std::llround(x0[r])) + ";");
       else line(std::string(VT()) + " " + xv(r) + " = " + lit(x0[r]) + ";");
     }
     for (int b = std::max(B - 1, 0); b < nbits; ++b) {
       const int j = K + b;
-      if (A.ptr[j + 1] == A.ptr[j]) continue;
+      bool any = false;
+      for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) any |= !dead_row(A.idx[p]);
+      if (!any) continue;
       std::string bn = "b" + std::to_string(b);
       if (i01) {
         line("const int " + bn + " = (int)((gr >> " + std::to_string(b) + ") & 1ull) << 1;");
-        for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) { ops += 1; line(xv(A.idx[p]) + " += " + bn + ";"); }
+        for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) {
+          if (dead_row(A.idx[p])) continue;
+          ops += 1;
+          line(xv(A.idx[p]) + " += " + bn + ";");
+        }
       } else {
         line("const double " + bn + " = __longlong_as_double((long long)(((gr >> " + std::to_string(b) +
              ") & 1ull) * 0x3FF0000000000000ull));");
         for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) {
+          if (dead_row(A.idx[p])) continue;
           ops += 1;
           line(xv(A.idx[p]) + " = fma(" + bn + ", " + lit(A.val[p]) + ", " + xv(A.idx[p]) + ");");
         }

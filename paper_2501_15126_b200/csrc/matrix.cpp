@@ -195,11 +195,12 @@ std::vector<int> costsort_swept(const Csx& ccs, const std::vector<int>& colp, in
   for (int k = 0; k < K; ++k)
     for (int p = ccs.ptr[colp[k]]; p < ccs.ptr[colp[k] + 1]; ++p) { grp[ccs.idx[p]] = k; gsize[k]++; }
   auto dcost = [](int k) { return k <= 1 ? 0 : (k == 2 ? 2 : 3 * k - 1); };
-  auto cost = [&](int c) {
-    int w = ccs.ptr[c + 1] - ccs.ptr[c];
+  auto cost = [&](int c) {  // rows of single-row groups are dead (never updated)
+    int w = 0;
     std::vector<char> seen(K, 0);
     for (int p = ccs.ptr[c]; p < ccs.ptr[c + 1]; ++p) {
       int g = grp[ccs.idx[p]];
+      if (g < 0 || gsize[g] > 1) ++w;
       if (g >= 0 && !seen[g]) { seen[g] = 1; w += dcost(gsize[g]); }
     }
     return w;

@@ -45,7 +45,8 @@ def main():
                     sw = min(ms)
                     steps = 2 ** (a.n - 1)
                     rate = i["w_plan"] * steps / (sw / 1e3)
-                    print(json.dumps({"n": a.n, "seed": seed, "Kreq": k, "K": i["K"], "B": i["B"], "U": i["U"],
+                    print(json.dumps({"n": a.n, "seed": seed, "Kreq": k, "minb": mb, "K": i["K"], "B": i["B"],
+                                      "U": i["U"], "order": i["ordering"], "var": i["swept_order"],
                                       "M": i["M"], "threads": th, "regs": i["regs_per_thread"],
                                       "bps": i["blocks_per_sm"], "warps_per_smsp": i["blocks_per_sm"] * th / 128,
                                       "w_plan": round(i["w_plan"], 4), "live": i["reg_rows"],
