@@ -6,7 +6,7 @@
 // P:224-262); hybrid mode keeps the rows of columns >= c in global
 // memory with a cached global product (Sec. V).
 //
-// B200 design generated here (DESIGN.md "Kernel"):
+// B200 design generated here (DESIGN.md section 3):
 //  * Factored columns 0..K-1 (pairwise row-disjoint, chosen by the planner):
 //    for fixed states of all other columns, the sum over the 2^K states of
 //    these columns of (-1)^|S| prod_i y_i factorises exactly into
@@ -32,6 +32,12 @@
 //    "global" rows: they need no storage at all during the sweep).
 //  * Bit 0 flips on every odd h-step; the two products of a pair differ only
 //    in Q_0, so a pair contributes (Q_0(even) - Q_0(odd)) * S_(above 0).
+//  * Value numbering: every straight-line region (seed, block body, each
+//    switch case) is emitted in SSA form with hash-consed subexpressions, so
+//    unchanged sub-products are reused instead of recomputed and every
+//    emitted arithmetic op is exactly one executed instruction (the kernel is
+//    compiled with --fmad=false; fusions are explicit).  W_plan therefore
+//    counts executed DADD/DMUL/DFMA.
 //  * Each chunk is seeded exactly from x0 + the swept columns of Gray(h0)
 //    (Sec. II-A), which bounds incremental x drift to 2^B steps.
 //  * Lane partials: pairwise inside a block, sequential over blocks and chunks,
@@ -39,8 +45,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <map>
 #include <set>
 #include <sstream>
+#include <tuple>
 
 #include "perm_internal.h"
 
@@ -48,7 +56,7 @@ namespace perm {
 
 namespace {
 
-std::string lit(double v) {  // exact hexadecimal floating literal
+std::string hexlit(double v) {  // exact hexadecimal floating literal
   char b[64];
   snprintf(b, sizeof b, "%a", v);
   return std::string("(") + b + ")";
@@ -76,8 +84,16 @@ struct Gen {
   bool has_frozen = false;
   std::ostringstream o;
   double ops = 0;                        // arithmetic ops emitted in the current region
-  int tmp = 0;
   std::string ind = "";
+
+  // ---- value numbering (SSA within one straight-line region) ----------------
+  struct Val { char op; int a, b, c; char ty; std::string name; };
+  std::vector<Val> vals;
+  std::map<std::tuple<char, int, int, int>, int> memo;
+  std::map<std::string, int> leafs;      // leaf text -> id (literals, region-start registers)
+  std::map<std::string, int> cur;        // register -> current value id
+  std::set<std::string> dirty;
+  int tmp = 0;
 
   Gen(const Csx& a, const std::vector<double>& x, const KernelSpec& s)
       : A(a), S(s), x0(x), i01(s.mode == PERM_MODE_INT01), n(a.n), K(s.K), B(s.B), U(s.U) {
@@ -117,123 +133,168 @@ struct Gen {
 
   const char* PT() const { return i01 ? "u128" : "double"; }
   const char* VT() const { return i01 ? "int" : "double"; }
+  const char* tyname(char t) const { return t == 'i' ? "int" : (t == 'u' ? "u128" : "double"); }
+  char pty() const { return i01 ? 'u' : 'd'; }
+  char xty() const { return i01 ? 'i' : 'd'; }
   std::string xv(int r) const { return "x" + std::to_string(r); }
-  std::string pt(int r) const { return i01 ? "((u128)(i128)" + xv(r) + ")" : xv(r); }
   std::string dv(int f) const { return "D" + std::to_string(fac[f].col); }
+  bool dead_row(int r) const { return fac[fac_of_row[r]].constant(); }
 
   void line(const std::string& s) { o << ind << s << "\n"; }
 
-  std::string mul(const std::string& a, const std::string& b) {
-    if (b.empty()) return a;
-    if (a.empty()) return b;
-    ops += 1;
-    return "(" + a + " * " + b + ")";
+  // ---- VN primitives -----------------------------------------------------------
+  int leaf(const std::string& text, char ty) {
+    auto it = leafs.find(text);
+    if (it != leafs.end()) return it->second;
+    vals.push_back({'L', -1, -1, -1, ty, text});
+    return leafs[text] = (int)vals.size() - 1;
   }
-  std::string tree(std::vector<std::string> v) {
-    if (v.empty()) return "";
+  int lit(double v) { return leaf(hexlit(v), 'd'); }
+  int ilit(long long v) { return leaf(std::to_string(v), 'i'); }
+  int ulit(long long v) { return leaf("((u128)" + std::to_string(v) + ")", 'u'); }
+  const std::string& nm(int id) const { return vals[id].name; }
+  int reg(const std::string& r, char ty) {
+    auto it = cur.find(r);
+    if (it != cur.end()) return it->second;
+    return cur[r] = leaf(r, ty);
+  }
+  void set(const std::string& r, int id) {
+    cur[r] = id;
+    dirty.insert(r);
+  }
+  int mk(char op, int a, int b, int c = -1) {
+    if ((op == '+' || op == '*') && a > b) std::swap(a, b);
+    auto key = std::make_tuple(op, a, b, c);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    char ty = vals[a].ty;
+    std::string expr;
+    switch (op) {
+      case '+': expr = nm(a) + " + " + nm(b); break;
+      case '-': expr = nm(a) + " - " + nm(b); break;
+      case '*': expr = nm(a) + " * " + nm(b); break;
+      case 'f': expr = "fma(" + nm(a) + ", " + nm(b) + ", " + nm(c) + ")"; break;
+      case 'c': expr = "(u128)(i128)" + nm(a); ty = 'u'; break;
+      case 'h': expr = "2 * " + nm(a); break;  // int doubling (INT01)
+    }
+    if (op != 'c') ops += 1;
+    std::string name = "t" + std::to_string(tmp++);
+    line(std::string("const ") + tyname(ty) + " " + name + " = " + expr + ";");
+    vals.push_back({op, a, b, c, ty, name});
+    return memo[key] = (int)vals.size() - 1;
+  }
+  int add(int a, int b) { return mk('+', a, b); }
+  int sub(int a, int b) { return mk('-', a, b); }
+  int mul(int a, int b) {
+    if (a < 0) return b;
+    if (b < 0) return a;
+    return mk('*', a, b);
+  }
+  int prod(std::vector<int> v) {  // balanced tree in fixed (list) order
+    if (v.empty()) return -1;
     while (v.size() > 1) {
-      std::vector<std::string> w;
+      std::vector<int> w;
       for (size_t i = 0; i + 1 < v.size(); i += 2) w.push_back(mul(v[i], v[i + 1]));
       if (v.size() & 1) w.push_back(v.back());
       v.swap(w);
     }
     return v[0];
   }
-
-  // value expression of factor f (after recompute_factor for groups)
-  std::string fexpr(int f) const {
-    const Factor& F = fac[f];
-    if (!F.group) return pt(F.rows[0]);
-    if (F.constant()) return i01 ? std::string("((u128)2)") : lit(F.a[0]);
-    return dv(f);
+  void begin_region() {
+    memo.clear();
+    leafs.clear();
+    cur.clear();
+    dirty.clear();
   }
-  // D_k = prod(y + a) - prod(y); emitted inline (returns expression)
-  std::string dexpr(int f) {
+  void end_region() {  // write loop-carried registers back
+    for (const std::string& r : dirty) {
+      const int id = cur[r];
+      if (vals[id].op == 'L' && vals[id].name == r) continue;
+      line(r + " = " + nm(id) + ";");
+    }
+    dirty.clear();
+  }
+
+  // ---- factors, levels, products -------------------------------------------------
+  int xval(int r) { return reg(xv(r), xty()); }
+  int pval(int r) { return i01 ? mk('c', xval(r), -1) : xval(r); }  // row value as product type
+  int group_value(int f) {  // D_k = prod(y + a) - prod(y)
     const Factor& F = fac[f];
     const size_t k = F.rows.size();
     if (i01) {
-      if (k == 2) {  // (x1+2)(x2+2) - x1 x2 = 2 x1 + 2 x2 + 4 (x doubled, a = 1)
-        ops += 3;
-        return "((u128)(i128)(2 * " + xv(F.rows[0]) + " + 2 * " + xv(F.rows[1]) + " + 4))";
+      if (k == 2) {  // (x1+2)(x2+2) - x1 x2 = 2 (x1 + x2) + 4 (x doubled, a = 1)
+        int s = mk('h', add(xval(F.rows[0]), xval(F.rows[1])), -1);
+        return mk('c', add(s, ilit(4)), -1);
       }
-      std::vector<std::string> in, out;
+      std::vector<int> in, out;
       for (int r : F.rows) {
-        ops += 1;
-        in.push_back("((u128)(i128)(" + xv(r) + " + 2))");
-        out.push_back(pt(r));
+        in.push_back(mk('c', add(xval(r), ilit(2)), -1));
+        out.push_back(pval(r));
       }
-      std::string a = tree(in), b = tree(out);
-      ops += 1;
-      return "(" + a + " - " + b + ")";
+      return sub(prod(in), prod(out));
     }
-    if (k == 2) {  // a1 y2 + a2 y1 + a1 a2: two FMAs, no cancellation
-      ops += 2;
-      return "fma(" + lit(F.a[0]) + ", " + xv(F.rows[1]) + ", fma(" + lit(F.a[1]) + ", " + xv(F.rows[0]) + ", " +
-             lit(F.a[0] * F.a[1]) + "))";
-    }
-    std::vector<std::string> in, out;
+    if (k == 2)  // a1 y2 + a2 y1 + a1 a2: two FMAs, no cancellation
+      return mk('f', lit(F.a[0]), xval(F.rows[1]), mk('f', lit(F.a[1]), xval(F.rows[0]), lit(F.a[0] * F.a[1])));
+    std::vector<int> in, out;
     for (size_t q = 0; q < k; ++q) {
-      ops += 1;
-      in.push_back("(" + xv(F.rows[q]) + " + " + lit(F.a[q]) + ")");
-      out.push_back(xv(F.rows[q]));
+      in.push_back(add(xval(F.rows[q]), lit(F.a[q])));
+      out.push_back(xval(F.rows[q]));
     }
-    std::string a = tree(in), b = tree(out);
-    ops += 1;
-    return "(" + a + " - " + b + ")";
+    return sub(prod(in), prod(out));
   }
-  void recompute_factor(int f) {
+  int fval(int f) {  // current value of factor f
     const Factor& F = fac[f];
-    if (!F.group || F.constant()) return;
-    line(dv(f) + " = " + dexpr(f) + ";");
+    if (!F.group) return pval(F.rows[0]);
+    if (F.constant()) return i01 ? ulit(2) : lit(F.a[0]);
+    return reg(dv(f), pty());
   }
-
   bool qreg(int l) const { return G[l].size() >= 2; }
-  std::string qexpr(int l) const { return qreg(l) ? "Q" + std::to_string(l) : fexpr(G[l][0]); }
+  int qval(int l) { return qreg(l) ? reg("Q" + std::to_string(l), pty()) : fval(G[l][0]); }
   int next_level(int l) const {
     for (int m : nonempty)
       if (m > l) return m;
     return -1;
   }
   bool sreg(int l) const { return next_level(l) >= 0 || has_frozen; }
-  std::string sexpr(int l) const { return sreg(l) ? "S" + std::to_string(l) : qexpr(l); }
-  std::string above(int l) const {
+  int sval(int l) { return sreg(l) ? reg("S" + std::to_string(l), pty()) : qval(l); }
+  int above(int l) {  // -1 = the empty product
     int m = next_level(l);
-    if (m >= 0) return sexpr(m);
-    return has_frozen ? "F" : "";
+    if (m >= 0) return sval(m);
+    return has_frozen ? reg("F", pty()) : -1;
   }
-
   void recompute_q(int l) {
     if (!qreg(l)) return;
-    std::vector<std::string> v;
-    for (int f : G[l]) v.push_back(fexpr(f));
-    line("Q" + std::to_string(l) + " = " + tree(v) + ";");
+    std::vector<int> v;
+    for (int f : G[l]) v.push_back(fval(f));
+    set("Q" + std::to_string(l), prod(v));
   }
   void recompute_s(int l) {  // l >= 1
     if (!sreg(l)) return;
-    line("S" + std::to_string(l) + " = " + mul(qexpr(l), above(l)) + ";");
+    set("S" + std::to_string(l), mul(qval(l), above(l)));
+  }
+  void recompute_factor(int f) {
+    const Factor& F = fac[f];
+    if (!F.group || F.constant()) return;
+    set(dv(f), group_value(f));
   }
 
-  // a row of a single-row factored column only enters through D_k = a_rk:
-  // its y value is never needed (no register, no updates)
-  bool dead_row(int r) const { return fac[fac_of_row[r]].constant(); }
-
-  // one update y_r +-= a_rj.  sign: "+", "-" (static) or a runtime +-1 name
+  // one update y_r +-= a_rj.  sign: "+", "-" (static) or a runtime +-1 register
   void update(int r, double a, const std::string& sign) {
-    if (dead_row(r)) return;
-    ops += 1;
+    if (dead_row(r)) return;  // only enters through the constant D_k = a_rk
+    int x = xval(r), y;
     if (i01) {
-      if (sign == "+") line(xv(r) + " += 2;");
-      else if (sign == "-") line(xv(r) + " -= 2;");
-      else line(xv(r) + " += " + sign + ";");  // runtime sign register holds +-2
+      if (sign == "+") y = add(x, ilit(2));
+      else if (sign == "-") y = sub(x, ilit(2));
+      else y = add(x, reg(sign, 'i'));  // runtime sign register holds +-2
     } else {
-      if (sign == "+") line(xv(r) + " += " + lit(a) + ";");
-      else if (sign == "-") line(xv(r) + " -= " + lit(a) + ";");
-      else line(xv(r) + " = fma(" + sign + ", " + lit(a) + ", " + xv(r) + ");");
+      if (sign == "+") y = add(x, lit(a));
+      else if (sign == "-") y = sub(x, lit(a));
+      else y = mk('f', reg(sign, 'd'), lit(a), x);
     }
+    set(xv(r), y);
   }
 
-  // flip of swept bit b (column K+b); recompute touched factors, their levels
-  // and the suffix chain down to level `lowest_s` (1 inside pairs, else 1)
+  // flip of swept bit b (column K+b): touched factors, their levels, suffix chain
   void flip(int b, const std::string& sign) {
     const int j = K + b;
     std::set<int> facs, levels;
@@ -252,7 +313,7 @@ struct Gen {
 
   // ---- the block body: 2^U h-steps, pairs (2k, 2k+1) -------------------------
   void block_body() {
-    std::vector<std::string> stack(U + 1);
+    std::vector<int> stack(U + 1, -1);
     const int npairs = 1 << (U - 1);
     for (int k = 0; k < npairs; ++k) {
       const int u = 2 * k;
@@ -263,8 +324,7 @@ struct Gen {
       }
       // pair: product at even step u (current state), flip bit 0, product at u+1
       std::string sg0 = (U >= 2) ? ((((u + 1) >> 1) & 1) ? "-" : "+") : "sU";
-      std::string e = "e" + std::to_string(tmp++);
-      line(std::string("const ") + PT() + " " + e + " = " + qexpr(0) + ";");
+      const int e = qval(0);
       {
         const int j = K;
         std::set<int> facs;
@@ -275,49 +335,37 @@ struct Gen {
         for (int f : facs) recompute_factor(f);
         recompute_q(0);
       }
-      ops += 1;  // e - Q0
-      std::string d = "(" + e + " - " + qexpr(0) + ")";
-      std::string t = "t" + std::to_string(tmp++);
-      std::string v;
+      const int d = sub(e, qval(0));
+      const int ab = above(0);
+      int v;
       int lvl = 0;
       unsigned kk = (unsigned)k;
-      const std::string ab = above(0);
-      if ((kk & 1u) && !ab.empty() && !i01) {
-        // first merge of the pairwise tree fused with the pair product:
-        // t = fma(d, S_above, stack[0]) -- one DFMA (the kernel is compiled
-        // with --fmad=false, so every emitted op is exactly one instruction)
-        ops += 1;
-        line(std::string("const ") + PT() + " " + t + " = fma(" + d + ", " + ab + ", " + stack[0] + ");");
-        v = t;
+      if ((kk & 1u) && ab >= 0 && !i01) {
+        // first merge of the pairwise tree fused with the pair product (one DFMA)
+        v = mk('f', d, ab, stack[0]);
         kk >>= 1;
         ++lvl;
       } else {
-        line(std::string("const ") + PT() + " " + t + " = " + mul(d, ab) + ";");
-        v = t;
+        v = mul(d, ab);
       }
-      // pairwise (binary-counter) accumulation of the pair terms
-      while (kk & 1u) {
-        std::string w = "v" + std::to_string(tmp++);
-        ops += 1;
-        line(std::string("const ") + PT() + " " + w + " = " + stack[lvl] + " + " + v + ";");
-        v = w;
+      while (kk & 1u) {  // pairwise (binary-counter) accumulation of the pair terms
+        v = add(stack[lvl], v);
         kk >>= 1;
         ++lvl;
       }
       stack[lvl] = v;
     }
-    ops += 1;
-    line("cacc += " + stack[U - 1] + ";");
+    set("cacc", add(reg("cacc", pty()), stack[U - 1]));
   }
 
+  // seed: y = x0 + swept columns of Gray(h0); only bits >= B-1 can be set
   void seed() {
-    // y = x0 + swept columns of Gray(h0); only bits >= B-1 can be set (h0 = chunk << B)
     const int nbits = n - 1 - K;
     line("const u64 gr = h0 ^ (h0 >> 1);");
+    begin_region();
     for (int r = 0; r < n; ++r) {
       if (dead_row(r)) continue;
-      if (i01) line(std::string(VT()) + " " + xv(r) + " = " + std::to_string((long long)std::llround(x0[r])) + ";");
-      else line(std::string(VT()) + " " + xv(r) + " = " + lit(x0[r]) + ";");
+      cur[xv(r)] = i01 ? ilit(std::llround(x0[r])) : lit(x0[r]);
     }
     for (int b = std::max(B - 1, 0); b < nbits; ++b) {
       const int j = K + b;
@@ -327,38 +375,51 @@ struct Gen {
       std::string bn = "b" + std::to_string(b);
       if (i01) {
         line("const int " + bn + " = (int)((gr >> " + std::to_string(b) + ") & 1ull) << 1;");
-        for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) {
-          if (dead_row(A.idx[p])) continue;
-          ops += 1;
-          line(xv(A.idx[p]) + " += " + bn + ";");
-        }
+        for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p)
+          if (!dead_row(A.idx[p])) set(xv(A.idx[p]), add(xval(A.idx[p]), leaf(bn, 'i')));
       } else {
         line("const double " + bn + " = __longlong_as_double((long long)(((gr >> " + std::to_string(b) +
              ") & 1ull) * 0x3FF0000000000000ull));");
-        for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) {
-          if (dead_row(A.idx[p])) continue;
-          ops += 1;
-          line(xv(A.idx[p]) + " = fma(" + bn + ", " + lit(A.val[p]) + ", " + xv(A.idx[p]) + ");");
-        }
+        for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p)
+          if (!dead_row(A.idx[p]))
+            set(xv(A.idx[p]), mk('f', leaf(bn, 'd'), lit(A.val[p]), xval(A.idx[p])));
       }
     }
-    for (int f = 0; f < (int)fac.size(); ++f)
-      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0) line(std::string(PT()) + " " + dv(f) + ";");
+    // frozen product
+    int F = -1;
     if (has_frozen) {
-      std::vector<std::string> v;
+      std::vector<int> v;
       for (int f = 0; f < (int)fac.size(); ++f)
-        if (fac[f].level < 0) v.push_back(fac[f].group && !fac[f].constant() ? dexpr(f) : fexpr(f));
-      line(std::string("const ") + PT() + " F = " + tree(v) + ";");
+        if (fac[f].level < 0) v.push_back(fac[f].group && !fac[f].constant() ? group_value(f) : fval(f));
+      F = prod(v);
+      line(std::string("const ") + PT() + " F = " + nm(F) + ";");
+      cur["F"] = leaf("F", pty());
     }
+    // live groups, level products, suffix chain
+    std::vector<std::pair<std::string, int>> decl;
     for (int f = 0; f < (int)fac.size(); ++f)
-      if (fac[f].level >= 0) recompute_factor(f);
+      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0) cur[dv(f)] = group_value(f);
     for (int l : nonempty)
-      if (qreg(l)) line(std::string(PT()) + " Q" + std::to_string(l) + ";");
-    for (int l : nonempty)
-      if (l >= 1 && sreg(l)) line(std::string(PT()) + " S" + std::to_string(l) + ";");
-    for (int l : nonempty) recompute_q(l);
+      if (qreg(l)) {
+        std::vector<int> v;
+        for (int f : G[l]) v.push_back(fval(f));
+        cur["Q" + std::to_string(l)] = prod(v);
+      }
     for (auto it = nonempty.rbegin(); it != nonempty.rend(); ++it)
-      if (*it >= 1) recompute_s(*it);
+      if (*it >= 1 && sreg(*it)) cur["S" + std::to_string(*it)] = mul(qval(*it), above(*it));
+    // declare the loop-carried registers
+    for (int r = 0; r < n; ++r)
+      if (!dead_row(r) && fac[fac_of_row[r]].level >= 0)
+        line(std::string(VT()) + " " + xv(r) + " = " + nm(cur[xv(r)]) + ";");
+    for (int f = 0; f < (int)fac.size(); ++f)
+      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0)
+        line(std::string(PT()) + " " + dv(f) + " = " + nm(cur[dv(f)]) + ";");
+    for (int l : nonempty)
+      if (qreg(l)) line(std::string(PT()) + " Q" + std::to_string(l) + " = " + nm(cur["Q" + std::to_string(l)]) + ";");
+    for (int l : nonempty)
+      if (l >= 1 && sreg(l)) line(std::string(PT()) + " S" + std::to_string(l) + " = " + nm(cur["S" + std::to_string(l)]) + ";");
+    (void)F;
+    dirty.clear();
   }
 };
 
@@ -411,7 +472,6 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
   double ops_body = 0, ops_switch = 0;
   if (U == 0) {
     // B == 0: one product per chunk (h = chunk), everything frozen; sign (-1)^h
-    g.ops = 0;
     const std::string P = g.has_frozen ? std::string("F") : std::string("1");
     g.line("cacc = (chunk & 1ull) ? (" + std::string(g.PT()) + ")(0 - " + P + ") : " + P + ";");
   } else {
@@ -431,7 +491,9 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
         std::string save = g.ind;
         g.ind += "  ";
         g.ops = 0;
+        g.begin_region();
         g.flip(b, "s");
+        g.end_region();
         ops_switch += g.ops * (double)(1ull << (B - 1 - b));  // flips of bit b per chunk
         g.line("break; }");
         g.ind = save;
@@ -448,7 +510,9 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
     if (g.i01) g.line("const int sU = ((h >> " + std::to_string(U) + ") & 1ull) ? -2 : 2;");
     else g.line("const double sU = ((h >> " + std::to_string(U) + ") & 1ull) ? -1.0 : 1.0;");
     g.ops = 0;
+    g.begin_region();
     g.block_body();
+    g.end_region();
     ops_body = g.ops;
     g.ind = "      ";
     g.line("}");
