@@ -129,6 +129,8 @@ typedef struct {
   int regs_per_thread, local_bytes, smem_bytes;
   double plan_ms, codegen_ms, nvrtc_ms;
   int cubin_cached;       /* 1 if the cubin came from the in-process cache */
+  int plan_cached;        /* 1 if ordering/codegen/NVRTC came from the in-process
+                             planner cache (same CCS content and options) */
   int row_perm[64];       /* ordered row i = original row row_perm[i] */
   int col_perm[64];       /* ordered column j = original column col_perm[j] */
 } perm_plan_info;
@@ -170,6 +172,18 @@ int perm_fold_async(perm_plan_t p, const void *d_partials, int world, void *d_ou
 
 /* Size in bytes of one partial / result for this plan (8 FP64, 16 INT01). */
 int perm_partial_bytes(perm_plan_t p);
+
+/* Shard geometry (host only, works for no_device plans): warp-tasks
+ * [*first_task, *first_task + *ntasks) and the Gray-step range
+ * [*g_begin, *g_end) of Alg. 1 that shard `rank` of `world` covers.  The
+ * shards of a world partition [0, 2^(n-1)) into contiguous aligned ranges. */
+int perm_shard_range(perm_plan_t p, int rank, int world, uint64_t *first_task, uint64_t *ntasks,
+                     uint64_t *g_begin, uint64_t *g_end);
+
+/* Host reference of perm_fold for FP64 plans (no device): fixed-order
+ * pairwise fold of `world` unscaled partials times the scale
+ * 2(-1)^(n-1)(-1)^K.  NaN on error.  Same arithmetic as the fold kernel. */
+double perm_fold_host(perm_plan_t p, const double *partials, int world);
 
 /* Copy the per-warp-task partial sums of the LAST shard/compute call to host
  * memory (double[ntask] for FP64; 2*uint64 per task for INT01).  Task t covers

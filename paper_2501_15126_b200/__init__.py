@@ -212,6 +212,18 @@ class Plan:
     def fold_async(self, d_partials: int, world: int, d_out: int):
         perm_fold_async(self.handle, d_partials, world, d_out)
 
+    def shard_range(self, rank: int, world: int):
+        """(first_task, ntasks, g_begin, g_end) of shard `rank` of `world`."""
+        v = [ctypes.c_uint64() for _ in range(4)]
+        _check(_abi.lib().perm_shard_range(self.handle, rank, world, *[ctypes.byref(x) for x in v]),
+               "perm_shard_range")
+        return tuple(x.value for x in v)
+
+    def fold_host(self, partials) -> float:
+        arr = np.ascontiguousarray(np.asarray(partials, dtype=np.float64))
+        return _abi.lib().perm_fold_host(self.handle, arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                         len(arr))
+
     def last_timing(self):
         """(sweep_ms, reduce_ms) of the last launch, from the plan's CUDA events."""
         a, b = ctypes.c_double(), ctypes.c_double()

@@ -47,7 +47,7 @@ class perm_plan_info(ctypes.Structure):
                 ("w_alg1", ctypes.c_double), ("block", ctypes.c_int), ("grid", ctypes.c_int),
                 ("blocks_per_sm", ctypes.c_int), ("sms", ctypes.c_int), ("regs_per_thread", ctypes.c_int),
                 ("local_bytes", ctypes.c_int), ("smem_bytes", ctypes.c_int), ("plan_ms", ctypes.c_double),
-                ("codegen_ms", ctypes.c_double), ("nvrtc_ms", ctypes.c_double), ("cubin_cached", ctypes.c_int),
+                ("codegen_ms", ctypes.c_double), ("nvrtc_ms", ctypes.c_double), ("cubin_cached", ctypes.c_int), ("plan_cached", ctypes.c_int),
                 ("row_perm", ctypes.c_int * 64), ("col_perm", ctypes.c_int * 64)]
 
     def as_dict(self):
@@ -64,7 +64,7 @@ EXPORTS = ["perm_plan", "perm_plan_ex", "perm_compute", "perm_compute_ex", "perm
            "perm_compute_shard_async", "perm_fold", "perm_fold_async", "perm_partial_bytes",
            "perm_debug_task_partials", "perm_last_timing", "perm_plan_get_info", "perm_plan_source", "perm_plan_cubin",
            "perm_free", "perm_last_error", "perm_version", "perm_structural_rank", "perm_order",
-           "perm_partition", "perm_alg2_launch_parameters"]
+           "perm_partition", "perm_alg2_launch_parameters", "perm_shard_range", "perm_fold_host"]
 
 _lib = None
 
@@ -108,5 +108,9 @@ def lib():
                                  ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
     L.perm_alg2_launch_parameters.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
                                               ctypes.c_int]
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    L.perm_shard_range.argtypes = [P, ctypes.c_int, ctypes.c_int, u64p, u64p, u64p, u64p]
+    L.perm_fold_host.restype = ctypes.c_double
+    L.perm_fold_host.argtypes = [P, dp, ctypes.c_int]
     _lib = L
     return L

@@ -150,7 +150,9 @@ struct perm_plan_s {
 
 namespace {
 
-#define CUDA_TRY(x)                                                                      \
+std::map<std::string, perm_plan_s> g_plan_cache;  // guarded by g_cache_mu
+
+#define CUDA_TRY(x)                                                                    \
   do {                                                                                   \
     cudaError_t e_ = (x);                                                                \
     if (e_ != cudaSuccess) return fail(PERM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
@@ -240,7 +242,7 @@ int shard_range(perm_plan_s* p, int rank, int world, uint64_t& first, uint64_t& 
     first = count * rank;
   } else {
     count = (uint64_t)rank < T ? 1 : 0;
-    first = rank;
+    first = std::min<uint64_t>((uint64_t)rank, T);  // empty shards sit at the end
   }
   return PERM_OK;
 }
@@ -402,7 +404,31 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     return x0;
   };
   std::vector<double> x0;
+  // in-process planner cache: same matrix + planning options -> same plan
+  std::string pkey;
   {
+    auto app = [&](const void* d, size_t nb) { pkey.append((const char*)d, nb); };
+    const int hdr[] = {n, mode, (int)ord, p->opts.chunk_log2, p->opts.block_log2, p->opts.task_chunks,
+                       p->opts.factor_cols, p->opts.min_blocks, p->opts.threads_per_block};
+    app(hdr, sizeof hdr);
+    app(&gr, sizeof gr);
+    app(p->ccs.ptr.data(), p->ccs.ptr.size() * sizeof(int32_t));
+    app(p->ccs.idx.data(), p->ccs.idx.size() * sizeof(int32_t));
+    app(p->ccs.val.data(), p->ccs.val.size() * sizeof(double));
+  }
+  bool plan_hit = false;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_plan_cache.find(pkey);
+    if (it != g_plan_cache.end()) {
+      const perm_opts keep = p->opts;
+      *p = it->second;  // planning state only (device fields are empty in the cache)
+      p->opts = keep;
+      I.plan_cached = 1;
+      plan_hit = true;
+    }
+  }
+  if (!plan_hit) {
     const double tc = now_ms();
     // candidates: base ordering x K factored columns (greedy row-disjoint
     // picks in base order, DESIGN "Factored columns"); pick the lowest W_plan
@@ -415,7 +441,8 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     if (p->opts.chunk_log2 > 0) bcaps = {p->opts.chunk_log2};
     // FP64-pipe efficiency vs resident 128-thread blocks per SM (1 warp per
     // SMSP each); calibrated on B200.
-    auto eff = [](int bps) { return bps >= 4 ? 1.0 : bps == 3 ? 0.95 : bps == 2 ? 0.8 : 0.5; };
+    // (profiles/r1_calibration.md: 3 -> 2 blocks costs 0-5 %; 1 block ~ half)
+    auto eff = [](int bps) { return bps >= 3 ? 1.0 : bps == 2 ? 0.95 : 0.55; };
     auto bps_of = [&](int regs, int threads) {
       const int r8 = (std::max(regs, 16) + 7) / 8 * 8;
       return std::max(1, std::min(16, 65536 / (threads * r8)));
@@ -522,15 +549,18 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     }
     if (n == 1) p->trivial1 = true;
     I.codegen_ms = now_ms() - tc - I.nvrtc_ms;
-  }
-  I.w_alg1 = w_alg1(p->occs);
-  if (!p->singular && !p->trivial1) {
-    I.w_plan = p->code.w_plan;
-    I.reg_rows = p->code.live_rows;
-    I.tier_rows = p->code.tier_rows;
-    I.seed_rows = p->code.seed_rows;
-    I.levels = p->code.levels;
-    I.block = p->spec.threads;
+    I.w_alg1 = w_alg1(p->occs);
+    if (!p->singular && !p->trivial1) {
+      I.w_plan = p->code.w_plan;
+      I.reg_rows = p->code.live_rows;
+      I.tier_rows = p->code.tier_rows;
+      I.seed_rows = p->code.seed_rows;
+      I.levels = p->code.levels;
+      I.block = p->spec.threads;
+    }
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    if (g_plan_cache.size() > 256) g_plan_cache.clear();
+    g_plan_cache[pkey] = *p;
   }
   I.plan_ms = now_ms() - t0;
   if (!p->opts.no_device) {
@@ -548,6 +578,46 @@ int perm_plan(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx, co
 }
 
 int perm_partial_bytes(perm_plan_t p) { return p && p->is_u128 ? 16 : 8; }
+
+int perm_shard_range(perm_plan_t p, int rank, int world, uint64_t* first_task, uint64_t* ntasks,
+                     uint64_t* g_begin, uint64_t* g_end) {
+  if (!p || !first_task || !ntasks || !g_begin || !g_end) return fail(PERM_EINVAL, "NULL argument");
+  uint64_t first, count;
+  int st = shard_range(p, rank, world, first, count);
+  if (st) return st;
+  *first_task = first;
+  *ntasks = count;
+  if (p->trivial1 || p->singular) {  // no sweep: rank 0 owns the whole range
+    const uint64_t total = p->n >= 2 ? (1ull << (p->n - 1)) : 1;
+    *g_begin = rank == 0 ? 0 : total;
+    *g_end = total;
+    return PERM_OK;
+  }
+  const uint64_t Lg = ((32ull * (uint64_t)p->info.M) << p->info.B) << p->info.K;  // Gray steps per task
+  *g_begin = first * Lg;
+  *g_end = (first + count) * Lg;
+  return PERM_OK;
+}
+
+double perm_fold_host(perm_plan_t p, const double* partials, int world) {
+  if (!p || !partials || p->is_u128 || world < 1 || world > 128 || (world & (world - 1))) {
+    g_err = "perm_fold_host: FP64 plan and power-of-two world <= 128 required";
+    return std::nan("");
+  }
+  if (p->singular) return 0.0;
+  const int nn = p->trivial1 ? 1 : p->n;
+  double st[8];  // same binary-counter pairwise tree as fold_f64 (reduce.cu)
+  for (int k = 0; k < world; ++k) {
+    double v = partials[k];
+    int lvl = 0, kk = k;
+    while (kk & 1) { v = st[lvl] + v; kk >>= 1; ++lvl; }
+    st[lvl] = v;
+  }
+  int top = 0;
+  while ((1 << top) < world) ++top;
+  const double scale = ((nn % 2) ? 2.0 : -2.0) * ((p->info.K & 1) ? -1.0 : 1.0);
+  return st[top] * scale;
+}
 
 int perm_compute_shard_async(perm_plan_t p, int rank, int world, void* d_partial) {
   if (!p) return fail(PERM_EINVAL, "plan is NULL");

@@ -1,0 +1,53 @@
+"""Multi-GPU plumbing (one process per GPU, torch.distributed over NCCL).
+
+The Gray range is split into `world` power-of-two-aligned shards of whole
+warp-tasks (perm_shard_range); each rank sweeps its shard on its own GPU
+(perm_compute_shard_async writes the 8/16-byte unscaled partial into a device
+tensor), one all-gather moves the partials (the path's single exchange step),
+and every rank folds them in rank order with the deterministic fold kernel
+(perm_fold_async), so the result is bitwise identical to the one-GPU result.
+"""
+from __future__ import annotations
+
+
+class ShardedPermanent:
+    """Buffers + one-call step for a plan across the ranks of `group`."""
+
+    def __init__(self, plan, rank: int, world: int, device, group=None):
+        import torch
+        self.plan, self.rank, self.world, self.group = plan, rank, world, group
+        self.words = plan.partial_bytes // 8           # 1 (FP64) or 2 (INT01) 8-byte words
+        self.part = torch.zeros(2, dtype=torch.float64, device=device)
+        self.gathered = torch.zeros(2 * world, dtype=torch.float64, device=device)
+        self.out = torch.zeros(2, dtype=torch.float64, device=device)
+
+    def step(self):
+        """Enqueue shard sweep + all-gather + fold on the current stream."""
+        import torch.distributed as dist
+        self.plan.shard_async(self.rank, self.world, self.part.data_ptr())
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.gathered[: self.world * self.words], self.part[: self.words],
+                                        group=self.group)
+            src = self.gathered
+        else:
+            src = self.part
+        self.plan.fold_async(src.data_ptr(), self.world, self.out.data_ptr())
+        return self.out
+
+    def value(self) -> float:
+        return float(self.out[0].item())
+
+
+def gather_fold_host(plan, partial: float, world: int, group=None) -> float:
+    """Host-side variant (CPU / gloo): all-gather one FP64 partial per rank and
+    fold with perm_fold_host (same fixed order and scale as the fold kernel)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([partial], dtype=torch.float64)
+    if world > 1:
+        out = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(out, t, group=group)
+        parts = [float(x.item()) for x in out]
+    else:
+        parts = [partial]
+    return plan.fold_host(parts)
