@@ -80,7 +80,11 @@ struct Gen {
   std::vector<Factor> fac;
   std::vector<int> fac_of_row;
   std::vector<std::vector<int>> G;       // factor ids per level
-  std::vector<int> nonempty;             // ascending levels
+  std::vector<int> nonempty;             // ascending register levels (< cT)
+  std::vector<int> tier_levels;          // HYBRID: nonempty levels >= cT (global tier)
+  int cT = 0;                            // first tier level (B: no tier)
+  std::vector<int> tier_slot;            // row -> tier slot or -1
+  std::map<std::string, int> tier_of;    // register name -> tier slot
   bool has_frozen = false;
   std::ostringstream o;
   double ops = 0;                        // arithmetic ops emitted in the current region
@@ -127,9 +131,23 @@ struct Gen {
       if (fac[f].level >= 0) G[fac[f].level].push_back(f);
       else has_frozen = true;
     }
+    // HYBRID (Sec. V): factors first flipped by bits >= cT keep their
+    // rows in a per-thread global tier; cT >= U so the tier is touched only by
+    // the block-boundary flips
+    cT = (S.mode == PERM_MODE_HYBRID && S.hybrid_c > 0) ? std::max(std::min(S.hybrid_c, B), std::min(U, B)) : B;
     for (int l = 0; l < B; ++l)
-      if (!G[l].empty()) nonempty.push_back(l);
+      if (!G[l].empty()) (l < cT ? nonempty : tier_levels).push_back(l);
+    tier_slot.assign(n, -1);
+    int slots = 0;
+    for (int l : tier_levels)
+      for (int f : G[l])
+        for (int r : fac[f].rows) {
+          tier_slot[r] = slots++;
+          tier_of[xv(r)] = tier_slot[r];
+        }
   }
+  bool has_tier() const { return !tier_levels.empty(); }
+  bool tierf(int f) const { return fac[f].level >= cT; }
 
   const char* PT() const { return i01 ? "u128" : "double"; }
   const char* VT() const { return i01 ? "int" : "double"; }
@@ -206,9 +224,14 @@ struct Gen {
     cur.clear();
     dirty.clear();
   }
-  void end_region() {  // write loop-carried registers back
+  void end_region() {  // write loop-carried registers (and tier rows) back
     for (const std::string& r : dirty) {
       const int id = cur[r];
+      auto t = tier_of.find(r);
+      if (t != tier_of.end()) {
+        line("TIER(" + std::to_string(t->second) + ") = " + nm(id) + ";");
+        continue;
+      }
       if (vals[id].op == 'L' && vals[id].name == r) continue;
       line(r + " = " + nm(id) + ";");
     }
@@ -216,7 +239,15 @@ struct Gen {
   }
 
   // ---- factors, levels, products -------------------------------------------------
-  int xval(int r) { return reg(xv(r), xty()); }
+  int xval(int r) {
+    if (tier_slot[r] < 0) return reg(xv(r), xty());
+    auto it = cur.find(xv(r));
+    if (it != cur.end()) return it->second;
+    std::string name = "t" + std::to_string(tmp++);  // tier load (coalesced across lanes)
+    line(std::string("const ") + VT() + " " + name + " = TIER(" + std::to_string(tier_slot[r]) + ");");
+    vals.push_back({'M', -1, -1, -1, xty(), name});
+    return cur[xv(r)] = (int)vals.size() - 1;
+  }
   int pval(int r) { return i01 ? mk('c', xval(r), -1) : xval(r); }  // row value as product type
   int group_value(int f) {  // D_k = prod(y + a) - prod(y)
     const Factor& F = fac[f];
@@ -246,6 +277,7 @@ struct Gen {
     const Factor& F = fac[f];
     if (!F.group) return pval(F.rows[0]);
     if (F.constant()) return i01 ? ulit(2) : lit(F.a[0]);
+    if (tierf(f)) return group_value(f);  // tier groups are not cached in registers
     return reg(dv(f), pty());
   }
   bool qreg(int l) const { return G[l].size() >= 2; }
@@ -255,12 +287,20 @@ struct Gen {
       if (m > l) return m;
     return -1;
   }
-  bool sreg(int l) const { return next_level(l) >= 0 || has_frozen; }
+  bool sreg(int l) const { return next_level(l) >= 0 || has_frozen || has_tier(); }
   int sval(int l) { return sreg(l) ? reg("S" + std::to_string(l), pty()) : qval(l); }
   int above(int l) {  // -1 = the empty product
     int m = next_level(l);
     if (m >= 0) return sval(m);
+    if (has_tier()) return reg("SG", pty());  // the paper's globalProduct (tier x frozen)
     return has_frozen ? reg("F", pty()) : -1;
+  }
+  void recompute_sg() {  // product of every tier factor (rows loaded from the tier) and F
+    std::vector<int> v;
+    for (int l : tier_levels)
+      for (int f : G[l]) v.push_back(fval(f));
+    if (has_frozen) v.push_back(reg("F", pty()));
+    set("SG", prod(v));
   }
   void recompute_q(int l) {
     if (!qreg(l)) return;
@@ -274,7 +314,7 @@ struct Gen {
   }
   void recompute_factor(int f) {
     const Factor& F = fac[f];
-    if (!F.group || F.constant()) return;
+    if (!F.group || F.constant() || tierf(f)) return;
     set(dv(f), group_value(f));
   }
 
@@ -303,10 +343,18 @@ struct Gen {
       facs.insert(fac_of_row[A.idx[p]]);
     }
     for (int f : facs) recompute_factor(f);
-    for (int f : facs)
-      if (fac[f].level >= 0) levels.insert(fac[f].level);  // constant D_k: unchanged
+    bool tier_touched = false;
+    for (int f : facs) {
+      if (fac[f].level < 0) continue;  // constant D_k: unchanged
+      if (tierf(f)) tier_touched = true;
+      else levels.insert(fac[f].level);
+    }
     for (int l : levels) recompute_q(l);
     int h = levels.empty() ? -1 : *levels.rbegin();
+    if (tier_touched) {
+      recompute_sg();
+      h = nonempty.empty() ? -1 : nonempty.back();
+    }
     for (auto it = nonempty.rbegin(); it != nonempty.rend(); ++it)
       if (*it >= 1 && *it <= h) recompute_s(*it);
   }
@@ -396,9 +444,9 @@ struct Gen {
       cur["F"] = leaf("F", pty());
     }
     // live groups, level products, suffix chain
-    std::vector<std::pair<std::string, int>> decl;
     for (int f = 0; f < (int)fac.size(); ++f)
-      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0) cur[dv(f)] = group_value(f);
+      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f)) cur[dv(f)] = group_value(f);
+    if (has_tier()) recompute_sg();
     for (int l : nonempty)
       if (qreg(l)) {
         std::vector<int> v;
@@ -408,12 +456,15 @@ struct Gen {
     for (auto it = nonempty.rbegin(); it != nonempty.rend(); ++it)
       if (*it >= 1 && sreg(*it)) cur["S" + std::to_string(*it)] = mul(qval(*it), above(*it));
     // declare the loop-carried registers
-    for (int r = 0; r < n; ++r)
-      if (!dead_row(r) && fac[fac_of_row[r]].level >= 0)
-        line(std::string(VT()) + " " + xv(r) + " = " + nm(cur[xv(r)]) + ";");
+    for (int r = 0; r < n; ++r) {
+      if (dead_row(r) || fac[fac_of_row[r]].level < 0) continue;
+      if (tier_slot[r] >= 0) line("TIER(" + std::to_string(tier_slot[r]) + ") = " + nm(cur[xv(r)]) + ";");
+      else line(std::string(VT()) + " " + xv(r) + " = " + nm(cur[xv(r)]) + ";");
+    }
     for (int f = 0; f < (int)fac.size(); ++f)
-      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0)
+      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f))
         line(std::string(PT()) + " " + dv(f) + " = " + nm(cur[dv(f)]) + ";");
+    if (has_tier()) line(std::string(PT()) + " SG = " + nm(cur["SG"]) + ";");
     for (int l : nonempty)
       if (qreg(l)) line(std::string(PT()) + " Q" + std::to_string(l) + " = " + nm(cur["Q" + std::to_string(l)]) + ";");
     for (int l : nonempty)
@@ -447,11 +498,18 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
     << " mode=" << S.mode << "\n";
   o << "typedef unsigned long long u64;\n";
   if (g.i01) o << "typedef unsigned __int128 u128;\ntypedef __int128 i128;\n";
+  // HYBRID tier: row slot s of this thread at tier[s * (all threads) + thread]
+  // (the paper's coalesced x[nthreads * row + tid] layout, Listing 4)
+  o << "#define TIER(s) tier[(size_t)(s) * nt_ + gt_]\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << S.threads << ", " << S.min_blocks << ")\n"
     << kc.name << "(const u64 task_begin, const unsigned task_count, unsigned* __restrict__ counter, "
-    << g.PT() << "* __restrict__ slots)\n{\n";
+    << g.PT() << "* __restrict__ slots, " << g.VT() << "* __restrict__ tier)\n{\n";
   g.ind = "  ";
   g.line("const unsigned lane = threadIdx.x & 31u;");
+  if (g.has_tier()) {
+    g.line("const unsigned gt_ = blockIdx.x * blockDim.x + threadIdx.x;");
+    g.line("const unsigned nt_ = gridDim.x * blockDim.x;");
+  }
   g.line("for (;;) {");
   g.ind = "    ";
   g.line("unsigned t = 0;");
@@ -550,14 +608,18 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
   }
   kc.live_rows = live;
   kc.seed_rows = frozen_rows;
-  kc.tier_rows = 0;
+  int tier_rows = 0;
+  for (int r = 0; r < A.n; ++r) tier_rows += g.tier_slot[r] >= 0;
+  kc.tier_rows = tier_rows;
+  kc.tier_bytes = tier_rows * (g.i01 ? 4 : 8);
+  kc.live_rows = live - tier_rows;
   kc.levels = (int)g.nonempty.size();
   int qs = 0, ds = 0;
   for (int l : g.nonempty) qs += g.qreg(l) + (l >= 1 && g.sreg(l));
   for (const Factor& f : g.fac) ds += f.group && !f.constant() && f.level >= 0;
   const int wpv = g.i01 ? 1 : 2;   // 32-bit registers per x value
   const int wpp = g.i01 ? 4 : 2;   // per product value
-  kc.est_regs = live * wpv + (qs + ds) * wpp + (U + 2) * wpp + 28;
+  kc.est_regs = kc.live_rows * wpv + (qs + ds) * wpp + (U + 2) * wpp + 28;
   return kc;
 }
 

@@ -46,7 +46,7 @@ struct KernelSpec {
   int K = 0;                   // factored (pairwise row-disjoint) leading columns
   int B = 0, U = 0, M = 1;     // chunk log2, unrolled block log2, chunks per lane per task
   int mode = PERM_MODE_REG;    // REG / HYBRID / INT01
-  int hybrid_c = 0;            // HYBRID: levels >= hybrid_c live in the shared tier
+  int hybrid_c = 0;            // HYBRID: factors of levels >= hybrid_c live in the global tier
   int threads = 128;           // threads per block
   int min_blocks = 1;          // __launch_bounds__ second argument
   uint64_t nchunks_total = 0;  // 2^(n-1-B)
@@ -56,7 +56,7 @@ struct KernelCode {
   std::string source;
   std::string name = "perm_sweep";
   int live_rows = 0, tier_rows = 0, seed_rows = 0, levels = 0;
-  int smem_per_thread = 0;  // bytes of tier storage per thread
+  int tier_bytes = 0;       // bytes of global tier storage per thread (HYBRID)
   double ops_seed = 0, ops_block = 0, ops_chunk_total = 0;
   double w_plan = 0;        // arithmetic ops per Gray step
   int est_regs = 0;         // rough register estimate (for __launch_bounds__)

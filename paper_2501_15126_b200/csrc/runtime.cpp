@@ -144,6 +144,7 @@ struct perm_plan_s {
   unsigned* d_counter = nullptr;
   void* d_partial = nullptr;  // 16 bytes
   void* d_scratch = nullptr;  // fold scratch (world entries)
+  void* d_tier = nullptr;     // HYBRID global tier (tier_rows x resident threads)
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   uint64_t last_first = 0, last_count = 0;
 };
@@ -196,6 +197,11 @@ int load_device(perm_plan_s* p) {
     p->info.grid = bps * p->info.sms;
     const size_t sb = (p->is_u128 ? 16 : 8) * (size_t)p->info.tasks;
     CUDA_TRY(cudaMalloc(&p->d_slots, std::max<size_t>(sb, 16)));
+    if (p->code.tier_bytes > 0) {
+      const size_t tb = (size_t)p->code.tier_bytes * (size_t)p->info.grid * (size_t)p->spec.threads;
+      CUDA_TRY(cudaMalloc(&p->d_tier, tb));
+      p->info.smem_bytes = 0;
+    }
   }
   p->on_device = true;
   return PERM_OK;
@@ -214,7 +220,7 @@ int run_range(perm_plan_s* p, uint64_t first, uint64_t count, double* sweep_ms, 
   CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned), p->stream));
   unsigned long long tb = first;
   unsigned tc = (unsigned)count;
-  void* args[] = {&tb, &tc, &p->d_counter, &p->d_slots};
+  void* args[] = {&tb, &tc, &p->d_counter, &p->d_slots, &p->d_tier};
   const int grid = (int)std::min<uint64_t>((uint64_t)p->info.grid,
                                            (count * 32 + p->spec.threads - 1) / p->spec.threads);
   CUDA_TRY(cudaEventRecord(p->ev[0], p->stream));
@@ -347,7 +353,6 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
       return fail(PERM_ERANGE, "INT01: Bregman-Minc bound * 2^(n-1) may exceed 2^127");
     }
   }
-  if (mode == PERM_MODE_HYBRID) mode = PERM_MODE_REG;  // tier generator: see DESIGN.md (REG layout)
   I.mode = mode;
   p->is_u128 = mode == PERM_MODE_INT01;
 
@@ -381,6 +386,20 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     sp.threads = p->opts.threads_per_block > 0 ? p->opts.threads_per_block : 128;
     sp.nchunks_total = nchunks;
     return warp_chunks / M;  // tasks
+  };
+
+  // HYBRID: tier split from Alg. 4's c on the candidate's ordered matrix
+  // (columns 0..K-1 are factored, so swept bit b is column K+b), clamped to
+  // [U, B] so the tier is touched only at block-boundary flips
+  auto set_hybrid = [&](KernelSpec& sp, const Csx& o) {
+    if (mode != PERM_MODE_HYBRID) return;
+    int cbits = p->opts.hybrid_c;
+    if (cbits <= 0) {
+      int k4, c4;
+      partition_alg4(o, gr, 148, k4, c4);
+      cbits = c4 - sp.K;
+    }
+    sp.hybrid_c = std::max(std::min(cbits, sp.B), std::min(sp.U, sp.B));
   };
 
   // ---- ordering
@@ -467,6 +486,7 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
           for (int bc : bcaps) {
             KernelSpec sp;
             geometry(K, sp, bc);
+            set_hybrid(sp, o);
             if (bc != bcaps[0] && sp.B != bc) continue;  // cap not binding: duplicate
             KernelCode kc = generate_kernel(o, xo, sp);
             const double score = kc.w_plan / eff(bps_of(kc.est_regs, sp.threads));
@@ -490,6 +510,7 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
       std::vector<double> xo = make_x0(o);
       KernelSpec sp;
       uint64_t tasks = geometry(c.K, sp, c.bcap);
+      set_hybrid(sp, o);
       if (n == 1 || p->singular) {
         p->rowp = rp; p->colp = colp; p->occs = o; p->spec = sp; x0 = xo;
         I.ordering = c.base; I.tasks = tasks; I.K = c.K; I.swept_order = c.var;
@@ -518,6 +539,7 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
         else if (sp.B > 2 && p->opts.chunk_log2 == 0) {
           const int keepU = sp.U;  // geometry() keeps min_blocks
           tasks = geometry(c.K, sp, sp.B - 2);
+          set_hybrid(sp, o);
           sp.U = std::min(keepU, sp.B);
         } else break;
       }
@@ -783,6 +805,7 @@ void perm_free(perm_plan_t p) {
     if (p->d_counter) cudaFree(p->d_counter);
     if (p->d_partial) cudaFree(p->d_partial);
     if (p->d_scratch) cudaFree(p->d_scratch);
+    if (p->d_tier) cudaFree(p->d_tier);
     for (auto& e : p->ev)
       if (e) cudaEventDestroy(e);
     if (p->lib) cudaLibraryUnload(p->lib);

@@ -155,6 +155,18 @@ def test_codegen_compiles_without_spills(n, p, seed, mode):
             assert re.search(r"\bD(ADD|MUL|FMA)\b", sass)
 
 
+def test_hybrid_codegen_uses_coalesced_tier():
+    A = synth.erdos_renyi(36, 0.2, 1)
+    P = pb.Plan.from_dense(A, mode="hybrid", factor_cols=-1, no_device=True)
+    i = P.info
+    assert i["mode"] == 2 and i["tier_rows"] > 0 and i["local_bytes"] == 0
+    src = P.source
+    assert "#define TIER(s) tier[(size_t)(s) * nt_ + gt_]" in src   # x[nthreads*row + tid], Listing 4
+    assert "SG" in src                                              # cached tier product (globalProduct)
+    R = pb.Plan.from_dense(A, mode="reg", factor_cols=-1, no_device=True)
+    assert i["regs_per_thread"] < R.info["regs_per_thread"]
+
+
 def test_codegen_literals_are_exact_hex():
     # Listing 2 analogue: the column-0 values appear as exact literals
     A = np.zeros((6, 6))

@@ -255,6 +255,27 @@ def test_int01_factored_vs_plain(n, seed):
         assert plan(A, mode="int01", factor_cols=fc).exact() == e
 
 
+@pytest.mark.parametrize("n,p,seed", [(20, 0.3, 1), (26, 0.25, 2), (30, 0.3, 1)])
+def test_hybrid_tier_vs_oracle(n, p, seed):
+    """HYBRID (Sec. V / Alg. 4 partition): rows first flipped by bits >= c in
+    the coalesced global tier; same value as REG and the oracle."""
+    A = synth.erdos_renyi(n, p, seed)
+    exp = oracle.perm_nw(A)[0]
+    for fc, hc in ((-1, 0), (-1, 6), (0, 0), (0, 7)):
+        P = plan(A, mode="hybrid", factor_cols=fc, hybrid_c=hc)
+        assert P.info["mode"] == 2
+        assert rel(P.compute(), exp) < 1e-11, (fc, hc, P.info["tier_rows"])
+
+
+def test_hybrid_has_tier_rows_at_n36():
+    A = synth.erdos_renyi(36, 0.2, 1)
+    P = plan(A, mode="hybrid", factor_cols=-1)
+    assert P.info["tier_rows"] > 0
+    R = plan(A, mode="reg", factor_cols=-1)
+    assert rel(P.compute(), R.compute()) < 1e-12
+    check_task_partials(A, P, 3)
+
+
 def test_repeatable_bitwise():
     A = synth.erdos_renyi(28, 0.2, 4)
     P = plan(A)
