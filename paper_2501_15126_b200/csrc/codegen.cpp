@@ -62,13 +62,23 @@ std::string hexlit(double v) {  // exact hexadecimal floating literal
   return std::string("(") + b + ")";
 }
 
-struct Factor {
-  bool group = false;          // D_k group of factored column `col`
-  int col = -1;                // factored column (group)
-  std::vector<int> rows;       // 1 row for a plain factor
-  std::vector<double> a;       // group: a_rk per row
+// Elimination tree: eliminating column c merges the factors it touches (T(c))
+// into one node E_c = prod_{f in T(c)} f(y + a_c) - prod_{f in T(c)} f(y).
+struct Node {
+  bool leaf = true;
+  int row = -1;                // leaf
+  int col = -1;                // internal: eliminated (ordered) column
+  std::vector<int> ch;         // internal: children node ids
+};
+
+struct Factor {                // a top-level factor (root of an elimination tree)
+  bool group = false;          // internal root (composite) vs plain row
+  int col = -1;                // group: its eliminated column (names the register)
+  int node = -1;
+  std::vector<int> rows;       // every row under the root
+  bool is_const = false;       // single-leaf elimination: value a_rc, y unused
   int level = -1;              // -1: frozen (no in-chunk bit touches it)
-  bool constant() const { return group && rows.size() == 1; }
+  bool constant() const { return is_const; }
 };
 
 struct Gen {
@@ -99,27 +109,54 @@ struct Gen {
   std::set<std::string> dirty;
   int tmp = 0;
 
+  std::vector<Node> nodes;
+  std::vector<std::map<int, double>> colval;  // ordered column -> (row -> a)
+
   Gen(const Csx& a, const std::vector<double>& x, const KernelSpec& s)
       : A(a), S(s), x0(x), i01(s.mode == PERM_MODE_INT01), n(a.n), K(s.K), B(s.B), U(s.U) {
-    fac_of_row.assign(n, -1);
-    for (int k = 0; k < K; ++k) {
-      Factor f;
-      f.group = true;
-      f.col = k;
-      for (int p = A.ptr[k]; p < A.ptr[k + 1]; ++p) {
-        f.rows.push_back(A.idx[p]);
-        f.a.push_back(A.val[p]);
-        fac_of_row[A.idx[p]] = (int)fac.size();
-      }
-      fac.push_back(f);
+    colval.assign(n, {});
+    for (int j = 0; j < n; ++j)
+      for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) colval[j][A.idx[p]] = A.val[p];
+    // replay the elimination of ordered columns 0..K-1
+    std::vector<int> root_of(n);          // row -> current root node
+    for (int r = 0; r < n; ++r) {
+      Node nd;
+      nd.row = r;
+      nodes.push_back(nd);
+      root_of[r] = r;
     }
-    for (int r = 0; r < n; ++r)
-      if (fac_of_row[r] < 0) {
+    for (int c = 0; c < K; ++c) {
+      std::set<int> T;
+      for (auto& kv : colval[c]) T.insert(root_of[kv.first]);
+      Node nd;
+      nd.leaf = false;
+      nd.col = c;
+      nd.ch.assign(T.begin(), T.end());
+      nodes.push_back(nd);
+      const int id = (int)nodes.size() - 1;
+      for (int r = 0; r < n; ++r)
+        if (T.count(root_of[r])) root_of[r] = id;
+    }
+    dead.assign(n, 0);  // the only child leaf of an elimination: value a_rc, y never read
+    for (const Node& nd : nodes)
+      if (!nd.leaf && nd.ch.size() == 1 && nodes[nd.ch[0]].leaf) dead[nodes[nd.ch[0]].row] = 1;
+    fac_of_row.assign(n, -1);
+    std::map<int, int> fac_of_root;
+    for (int r = 0; r < n; ++r) {
+      const int rt = root_of[r];
+      auto it = fac_of_root.find(rt);
+      if (it == fac_of_root.end()) {
         Factor f;
-        f.rows.push_back(r);
-        fac_of_row[r] = (int)fac.size();
+        f.node = rt;
+        f.group = !nodes[rt].leaf;
+        f.col = nodes[rt].col;
+        f.is_const = f.group && nodes[rt].ch.size() == 1 && nodes[nodes[rt].ch[0]].leaf;
+        it = fac_of_root.emplace(rt, (int)fac.size()).first;
         fac.push_back(f);
       }
+      fac[it->second].rows.push_back(r);
+      fac_of_row[r] = it->second;
+    }
     // level = lowest in-chunk swept bit whose column touches the factor
     for (int b = B - 1; b >= 0; --b) {
       const int j = K + b;
@@ -156,7 +193,8 @@ struct Gen {
   char xty() const { return i01 ? 'i' : 'd'; }
   std::string xv(int r) const { return "x" + std::to_string(r); }
   std::string dv(int f) const { return "D" + std::to_string(fac[f].col); }
-  bool dead_row(int r) const { return fac[fac_of_row[r]].constant(); }
+  std::vector<char> dead;
+  bool dead_row(int r) const { return dead[r]; }
 
   void line(const std::string& s) { o << ind << s << "\n"; }
 
@@ -249,34 +287,44 @@ struct Gen {
     return cur[xv(r)] = (int)vals.size() - 1;
   }
   int pval(int r) { return i01 ? mk('c', xval(r), -1) : xval(r); }  // row value as product type
-  int group_value(int f) {  // D_k = prod(y + a) - prod(y)
-    const Factor& F = fac[f];
-    const size_t k = F.rows.size();
-    if (i01) {
-      if (k == 2) {  // (x1+2)(x2+2) - x1 x2 = 2 (x1 + x2) + 4 (x doubled, a = 1)
-        int s = mk('h', add(xval(F.rows[0]), xval(F.rows[1])), -1);
-        return mk('c', add(s, ilit(4)), -1);
-      }
-      std::vector<int> in, out;
-      for (int r : F.rows) {
-        in.push_back(mk('c', add(xval(r), ilit(2)), -1));
-        out.push_back(pval(r));
-      }
-      return sub(prod(in), prod(out));
+  // value of elimination-tree node `id` with row shifts `sh` (ancestors'
+  // eliminated columns switched in; INT01 shifts in doubled units)
+  int node_value(int id, const std::map<int, double>& sh) {
+    const Node& N = nodes[id];
+    auto shift = [&](int r) { auto it = sh.find(r); return it == sh.end() ? 0.0 : it->second; };
+    if (N.leaf) {
+      const double s = shift(N.row);
+      if (i01) return s == 0 ? pval(N.row) : mk('c', add(xval(N.row), ilit(std::llround(s))), -1);
+      return s == 0 ? xval(N.row) : add(xval(N.row), lit(s));
     }
-    if (k == 2)  // a1 y2 + a2 y1 + a1 a2: two FMAs, no cancellation
-      return mk('f', lit(F.a[0]), xval(F.rows[1]), mk('f', lit(F.a[1]), xval(F.rows[0]), lit(F.a[0] * F.a[1])));
+    const std::map<int, double>& cv = colval[N.col];
+    if (N.ch.size() == 1 && nodes[N.ch[0]].leaf)  // (y + s + a) - (y + s) = a exactly
+      return i01 ? ulit(2) : lit(cv.at(nodes[N.ch[0]].row));
+    if (N.ch.size() == 2 && nodes[N.ch[0]].leaf && nodes[N.ch[1]].leaf) {
+      const int r1 = nodes[N.ch[0]].row, r2 = nodes[N.ch[1]].row;
+      const double s1 = shift(r1), s2 = shift(r2);
+      if (i01) {  // (x1+s1+2)(x2+s2+2) - (x1+s1)(x2+s2) = 2 (x1 + x2) + (2 s1 + 2 s2 + 4)
+        int t = mk('h', add(xval(r1), xval(r2)), -1);
+        return mk('c', add(t, ilit(std::llround(2 * s1 + 2 * s2 + 4))), -1);
+      }
+      // a1 (y2 + s2) + a2 (y1 + s1) + a1 a2: two FMAs, no cancellation
+      const double a1 = cv.at(r1), a2 = cv.at(r2);
+      return mk('f', lit(a1), xval(r2), mk('f', lit(a2), xval(r1), lit(a1 * a2 + a1 * s2 + a2 * s1)));
+    }
+    std::map<int, double> shin = sh;
+    for (auto& kv : cv) shin[kv.first] += i01 ? 2.0 : kv.second;
     std::vector<int> in, out;
-    for (size_t q = 0; q < k; ++q) {
-      in.push_back(add(xval(F.rows[q]), lit(F.a[q])));
-      out.push_back(xval(F.rows[q]));
+    for (int c : N.ch) {
+      in.push_back(node_value(c, shin));
+      out.push_back(node_value(c, sh));
     }
     return sub(prod(in), prod(out));
   }
+  int group_value(int f) { return node_value(fac[f].node, {}); }
   int fval(int f) {  // current value of factor f
     const Factor& F = fac[f];
     if (!F.group) return pval(F.rows[0]);
-    if (F.constant()) return i01 ? ulit(2) : lit(F.a[0]);
+    if (F.constant()) return group_value(f);  // literal a_rc
     if (tierf(f)) return group_value(f);  // tier groups are not cached in registers
     return reg(dv(f), pty());
   }

@@ -6,7 +6,9 @@
 #include <climits>
 #include <functional>
 #include <cmath>
+#include <map>
 #include <queue>
+#include <set>
 
 #include "perm_internal.h"
 
@@ -189,19 +191,59 @@ std::vector<int> factored_columns(const std::vector<int>& base_colp, const std::
   return out;
 }
 
+int elim_eval_size(const Csx& ccs, const std::vector<int>& colp, int K) {
+  // leaf = 1; elimination node = 2 x sum(children) (evaluated at the in and
+  // out states); returns the largest root -- bounds generated code size
+  const int n = ccs.n;
+  std::vector<int> root(n);
+  std::map<int, long long> size;
+  for (int r = 0; r < n; ++r) { root[r] = r; size[r] = 1; }
+  long long worst = 1;
+  int next = n;
+  for (int k = 0; k < K; ++k) {
+    const int c = colp[k];
+    std::set<int> T;
+    for (int p = ccs.ptr[c]; p < ccs.ptr[c + 1]; ++p) T.insert(root[ccs.idx[p]]);
+    long long s = 0;
+    for (int t : T) s += size[t];
+    const int id = next++;
+    size[id] = std::min<long long>(2 * s, 1ll << 40);
+    worst = std::max(worst, size[id]);
+    for (int r = 0; r < n; ++r)
+      if (T.count(root[r])) root[r] = id;
+  }
+  return (int)std::min<long long>(worst, 1 << 30);
+}
+
 std::vector<int> costsort_swept(const Csx& ccs, const std::vector<int>& colp, int K) {
   const int n = ccs.n;
-  std::vector<int> grp(n, -1), gsize(K, 0);
-  for (int k = 0; k < K; ++k)
-    for (int p = ccs.ptr[colp[k]]; p < ccs.ptr[colp[k] + 1]; ++p) { grp[ccs.idx[p]] = k; gsize[k]++; }
-  auto dcost = [](int k) { return k <= 1 ? 0 : (k == 2 ? 2 : 3 * k - 1); };
-  auto cost = [&](int c) {  // rows of single-row groups are dead (never updated)
+  // replay the eliminations of colp[0..K): root per row, dead rows (the only
+  // row of an elimination), live rows under each composite root
+  std::vector<int> root(n);
+  for (int r = 0; r < n; ++r) root[r] = r;
+  std::vector<char> dead(n, 0), composite(2 * n + K + 1, 0);
+  int next = n;
+  for (int k = 0; k < K; ++k) {
+    const int c = colp[k];
+    std::set<int> T;
+    for (int p = ccs.ptr[c]; p < ccs.ptr[c + 1]; ++p) T.insert(root[ccs.idx[p]]);
+    if (T.size() == 1 && *T.begin() < n && ccs.ptr[c + 1] - ccs.ptr[c] == 1) dead[*T.begin()] = 1;
+    const int id = next++;
+    composite[id] = 1;
+    for (int r = 0; r < n; ++r)
+      if (T.count(root[r])) root[r] = id;
+  }
+  std::map<int, int> live;
+  for (int r = 0; r < n; ++r)
+    if (!dead[r]) live[root[r]]++;
+  auto cost = [&](int c) {  // live rows updated + rough recompute cost of touched composites
     int w = 0;
-    std::vector<char> seen(K, 0);
+    std::set<int> seen;
     for (int p = ccs.ptr[c]; p < ccs.ptr[c + 1]; ++p) {
-      int g = grp[ccs.idx[p]];
-      if (g < 0 || gsize[g] > 1) ++w;
-      if (g >= 0 && !seen[g]) { seen[g] = 1; w += dcost(gsize[g]); }
+      const int r = ccs.idx[p];
+      if (dead[r]) continue;
+      ++w;
+      if (composite[root[r]] && seen.insert(root[r]).second) w += 2 * live[root[r]];
     }
     return w;
   };

@@ -33,6 +33,9 @@ std::vector<int> factor_picks(const Csx& ccs, const std::vector<int>& base_colp,
 // column order with the first K picks moved to the front (pick order), the
 // other columns in base order (the base's last column stays last).
 std::vector<int> factored_columns(const std::vector<int>& base_colp, const std::vector<int>& picks, int K);
+// largest elimination-tree evaluation size after eliminating colp[0..K)
+// (leaf 1, node 2 x sum of children)
+int elim_eval_size(const Csx& ccs, const std::vector<int>& colp, int K);
 // swept columns (positions K..n-2) stably sorted by flip cost
 // nnz(c) + sum over touched factored groups g of dcost(|g|) (0, 2, 3|g|-1)
 std::vector<int> costsort_swept(const Csx& ccs, const std::vector<int>& colp, int K);

@@ -474,10 +474,54 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
       std::vector<int> c = factored_columns(cp, picks, K);
       return var ? costsort_swept(p->ccs, c, K) : c;
     };
+    // Elimination sequence per base ordering: greedy, each step
+    // takes the candidate column whose elimination lowers the generated
+    // code's exact FP64 op count per Gray step the most (evaluated on a
+    // reduced geometry), until no candidate helps.
+    auto greedy_elim = [&](const std::vector<int>& rp, const std::vector<int>& cp) {
+      std::vector<int> seq;
+      if (kcap == 0) return seq;
+      auto evalW = [&](const std::vector<int>& s) {
+        const int k = (int)s.size();
+        std::vector<int> c = costsort_swept(p->ccs, factored_columns(cp, s, k), k);
+        Csx o = permute_ccs(p->ccs, rp, c);
+        KernelSpec sp;
+        geometry(k, sp, 8);
+        sp.U = std::min(sp.U, 4);
+        set_hybrid(sp, o);
+        return generate_kernel(o, make_x0(o), sp).w_plan;
+      };
+      double cur = evalW(seq);
+      while ((int)seq.size() < kcap && (int)seq.size() < n - 3) {
+        const int k = (int)seq.size();
+        std::vector<int> cand;
+        std::vector<int> fc = factored_columns(cp, seq, k);
+        for (int q = k; q < n - 1 && (int)cand.size() < 6; ++q) cand.push_back(fc[q]);
+        std::vector<int> cs = costsort_swept(p->ccs, fc, k);
+        for (int q = k, added = 0; q < n - 1 && added < 6; ++q, ++added)
+          if (std::find(cand.begin(), cand.end(), cs[q]) == cand.end()) cand.push_back(cs[q]);
+        double bw = 1e300;
+        int bc = -1;
+        for (int c : cand) {
+          std::vector<int> s2 = seq;
+          s2.push_back(c);
+          // bound the composite factors' evaluation size (code size, registers)
+          if (elim_eval_size(p->ccs, factored_columns(cp, s2, k + 1), k + 1) > 48) continue;
+          const double w = evalW(s2);
+          if (w < bw) { bw = w; bc = c; }
+        }
+        if (bc < 0 || !(bw < cur * 0.995)) break;
+        seq.push_back(bc);
+        cur = bw;
+      }
+      return seq;
+    };
+    std::map<int, std::vector<int>> elim_of_base;
     for (int base : bases) {
       std::vector<int> rp, cp;
       order_with(base, rp, cp);
-      std::vector<int> picks = factor_picks(p->ccs, cp, kcap);
+      std::vector<int> picks = greedy_elim(rp, cp);
+      elim_of_base[base] = picks;
       const int kmax = (int)picks.size();
       for (int K = (p->opts.factor_cols > 0 ? kmax : 0); K <= kmax; ++K)
         for (int var = 0; var < nvar; ++var) {
@@ -504,7 +548,7 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     for (const Cand& c : cands) {
       std::vector<int> rp, cp;
       order_with(c.base, rp, cp);
-      std::vector<int> picks = factor_picks(p->ccs, cp, kcap);
+      const std::vector<int>& picks = elim_of_base[c.base];
       std::vector<int> colp = colp_of(cp, picks, c.K, c.var);
       Csx o = permute_ccs(p->ccs, rp, colp);
       std::vector<double> xo = make_x0(o);
