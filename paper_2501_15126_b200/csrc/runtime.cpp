@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <map>
 #include <mutex>
 #include <string>
@@ -478,6 +479,9 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     // takes the candidate column whose elimination lowers the generated
     // code's exact FP64 op count per Gray step the most (evaluated on a
     // reduced geometry), until no candidate helps.
+    // search knobs (env overrides for tuning experiments)
+    const int elim_cands = getenv("PERM_ELIM_CANDS") ? atoi(getenv("PERM_ELIM_CANDS")) : 6;
+    const int elim_maxsize = getenv("PERM_ELIM_MAXSIZE") ? atoi(getenv("PERM_ELIM_MAXSIZE")) : 96;
     auto greedy_elim = [&](const std::vector<int>& rp, const std::vector<int>& cp) {
       std::vector<int> seq;
       if (kcap == 0) return seq;
@@ -496,19 +500,23 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
         const int k = (int)seq.size();
         std::vector<int> cand;
         std::vector<int> fc = factored_columns(cp, seq, k);
-        for (int q = k; q < n - 1 && (int)cand.size() < 6; ++q) cand.push_back(fc[q]);
+        for (int q = k; q < n - 1 && (int)cand.size() < elim_cands; ++q) cand.push_back(fc[q]);
         std::vector<int> cs = costsort_swept(p->ccs, fc, k);
-        for (int q = k, added = 0; q < n - 1 && added < 6; ++q, ++added)
+        for (int q = k, added = 0; q < n - 1 && added < elim_cands; ++q, ++added)
           if (std::find(cand.begin(), cand.end(), cs[q]) == cand.end()) cand.push_back(cs[q]);
         double bw = 1e300;
         int bc = -1;
+        std::vector<std::pair<int, std::future<double>>> jobs;  // candidates evaluated concurrently
         for (int c : cand) {
           std::vector<int> s2 = seq;
           s2.push_back(c);
           // bound the composite factors' evaluation size (code size, registers)
-          if (elim_eval_size(p->ccs, factored_columns(cp, s2, k + 1), k + 1) > 48) continue;
-          const double w = evalW(s2);
-          if (w < bw) { bw = w; bc = c; }
+          if (elim_eval_size(p->ccs, factored_columns(cp, s2, k + 1), k + 1) > elim_maxsize) continue;
+          jobs.emplace_back(c, std::async(std::launch::async, evalW, s2));
+        }
+        for (auto& j : jobs) {
+          const double w = j.second.get();
+          if (w < bw) { bw = w; bc = j.first; }
         }
         if (bc < 0 || !(bw < cur * 0.995)) break;
         seq.push_back(bc);
@@ -545,58 +553,78 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     // the best by W_plan / eff(actual registers)
     double best_score = 1e300;
     bool have = false;
-    for (const Cand& c : cands) {
-      std::vector<int> rp, cp;
-      order_with(c.base, rp, cp);
-      const std::vector<int>& picks = elim_of_base[c.base];
-      std::vector<int> colp = colp_of(cp, picks, c.K, c.var);
-      Csx o = permute_ccs(p->ccs, rp, colp);
-      std::vector<double> xo = make_x0(o);
+    struct Built {
+      int status = PERM_OK;
+      std::string err;
+      bool ok = false;
+      std::vector<int> rp, colp;
+      Csx o;
+      std::vector<double> xo;
       KernelSpec sp;
-      uint64_t tasks = geometry(c.K, sp, c.bcap);
-      set_hybrid(sp, o);
-      if (n == 1 || p->singular) {
-        p->rowp = rp; p->colp = colp; p->occs = o; p->spec = sp; x0 = xo;
-        I.ordering = c.base; I.tasks = tasks; I.K = c.K; I.swept_order = c.var;
-        have = true;
-        break;
-      }
+      uint64_t tasks = 0;
       KernelCode kc;
       std::vector<char> cubin;
       std::string log;
-      int regs = -1, stack = 0, spill = 0;
-      sp.min_blocks = p->opts.min_blocks > 0 ? p->opts.min_blocks
-                                             : bps_of(generate_kernel(o, xo, sp).est_regs + 16, sp.threads);
+      int regs = -1;
+      double nvrtc_ms = 0;
+      bool cached = false;
+    };
+    // one candidate: codegen + NVRTC with the spill gate and escalation
+    auto build = [&](const Cand& c) {
+      Built b;
+      std::vector<int> cp;
+      order_with(c.base, b.rp, cp);
+      b.colp = colp_of(cp, elim_of_base[c.base], c.K, c.var);
+      b.o = permute_ccs(p->ccs, b.rp, b.colp);
+      b.xo = make_x0(b.o);
+      b.tasks = geometry(c.K, b.sp, c.bcap);
+      set_hybrid(b.sp, b.o);
+      if (n == 1 || p->singular) { b.ok = true; return b; }
+      int stack = 0, spill = 0;
+      b.sp.min_blocks = p->opts.min_blocks > 0 ? p->opts.min_blocks
+                                               : bps_of(generate_kernel(b.o, b.xo, b.sp).est_regs + 16, b.sp.threads);
       for (int attempt = 0; attempt < 24; ++attempt) {
-        kc = generate_kernel(o, xo, sp);
-        bool cached = false;
+        b.kc = generate_kernel(b.o, b.xo, b.sp);
         double ms = 0;
-        st = nvrtc_compile(kc.source, cubin, log, p->is_u128, cached, ms);
-        if (st != PERM_OK) return bail(st);
-        I.nvrtc_ms += ms;
-        I.cubin_cached = cached;
-        parse_ptxas(log, regs, stack, spill);
-        if (stack <= 0 && spill <= 0) break;
+        b.status = nvrtc_compile(b.kc.source, b.cubin, b.log, p->is_u128, b.cached, ms);
+        if (b.status != PERM_OK) { b.err = g_err; return b; }
+        b.nvrtc_ms += ms;
+        parse_ptxas(b.log, b.regs, stack, spill);
+        if (stack <= 0 && spill <= 0) { b.ok = true; break; }
         // escalate: larger register cap, then a shorter unrolled block, then fewer chunk bits
-        if (sp.min_blocks > 1) sp.min_blocks -= 1;
-        else if (sp.U > 2) sp.U -= 1;
-        else if (sp.B > 2 && p->opts.chunk_log2 == 0) {
-          const int keepU = sp.U;  // geometry() keeps min_blocks
-          tasks = geometry(c.K, sp, sp.B - 2);
-          set_hybrid(sp, o);
-          sp.U = std::min(keepU, sp.B);
+        if (b.sp.min_blocks > 1) b.sp.min_blocks -= 1;
+        else if (b.sp.U > 2) b.sp.U -= 1;
+        else if (b.sp.B > 2 && p->opts.chunk_log2 == 0) {
+          const int keepU = b.sp.U;  // geometry() keeps min_blocks
+          b.tasks = geometry(c.K, b.sp, b.sp.B - 2);
+          set_hybrid(b.sp, b.o);
+          b.sp.U = std::min(keepU, b.sp.B);
         } else break;
       }
-      if (stack > 0 || spill > 0) continue;
-      const double score = kc.w_plan / eff(bps_of(regs, sp.threads));
+      return b;
+    };
+    std::vector<std::future<Built>> fut;  // candidates compiled concurrently (NVRTC is thread-safe)
+    for (const Cand& c : cands) fut.push_back(std::async(std::launch::async, build, c));
+    for (size_t ci = 0; ci < cands.size(); ++ci) {
+      Built b = fut[ci].get();
+      const Cand& c = cands[ci];
+      if (b.status != PERM_OK) {
+        for (size_t cj = ci + 1; cj < cands.size(); ++cj) fut[cj].wait();
+        g_err = b.err;
+        return bail(b.status);
+      }
+      I.nvrtc_ms += b.nvrtc_ms;
+      if (!b.ok) continue;
+      const double score = (n == 1 || p->singular) ? 0.0 : b.kc.w_plan / eff(bps_of(b.regs, b.sp.threads));
       if (!have || score < best_score) {
         have = true;
         best_score = score;
-        p->rowp = rp; p->colp = colp; p->occs = o; p->spec = sp; x0 = xo;
-        p->code = kc; p->cubin = cubin; p->ptxas_log = log;
-        I.ordering = c.base; I.tasks = tasks; I.K = c.K; I.swept_order = c.var;
-        I.regs_per_thread = regs;
+        p->rowp = b.rp; p->colp = b.colp; p->occs = b.o; p->spec = b.sp; x0 = b.xo;
+        p->code = b.kc; p->cubin = b.cubin; p->ptxas_log = b.log;
+        I.ordering = c.base; I.tasks = b.tasks; I.K = c.K; I.swept_order = c.var;
+        I.regs_per_thread = b.regs;
         I.local_bytes = 0;
+        I.cubin_cached = b.cached;
       }
     }
     if (!have) {
