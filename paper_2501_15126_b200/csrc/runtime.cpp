@@ -12,6 +12,7 @@
 #include <future>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -366,7 +367,10 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
   }
   auto geometry = [&](int K, KernelSpec& sp, int bcap) {
     const int nb = std::max(0, n - 1 - K);  // h-bits
-    int B = p->opts.chunk_log2 > 0 ? p->opts.chunk_log2 : std::min(bcap, std::max(0, nb - 5));
+    // at least 2^17 warp-tasks when the range allows (B >= 8): >= 14 tasks per
+    // resident warp on each of 8 GPUs keeps the dynamic-scheduling tail small
+    const int btask = std::max(8, nb - 5 - 17);
+    int B = p->opts.chunk_log2 > 0 ? p->opts.chunk_log2 : std::min(std::min(bcap, btask), std::max(0, nb - 5));
     if (B > nb) B = nb;
     int U = p->opts.block_log2 > 0 ? p->opts.block_log2 : 5;
     if (U > B) U = B;
@@ -375,7 +379,7 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     uint64_t M = p->opts.task_chunks > 0 ? (uint64_t)p->opts.task_chunks : 0;
     if (M == 0) {
       M = 1;
-      while (warp_chunks / (M * 2) >= (1ull << 16)) M *= 2;
+      while (warp_chunks / (M * 2) >= (1ull << 17)) M *= 2;
     }
     if (M > warp_chunks) M = warp_chunks;
     sp.n = n;
@@ -535,11 +539,12 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
         for (int var = 0; var < nvar; ++var) {
           Csx o = permute_ccs(p->ccs, rp, colp_of(cp, picks, K, var));
           std::vector<double> xo = make_x0(o);
+          std::set<int> seenB;
           for (int bc : bcaps) {
             KernelSpec sp;
             geometry(K, sp, bc);
             set_hybrid(sp, o);
-            if (bc != bcaps[0] && sp.B != bc) continue;  // cap not binding: duplicate
+            if (!seenB.insert(sp.B).second) continue;  // cap not binding: duplicate
             KernelCode kc = generate_kernel(o, xo, sp);
             const double score = kc.w_plan / eff(bps_of(kc.est_regs, sp.threads));
             cands.push_back({score, kc.w_plan, base, K, var, bc, kc.est_regs});
