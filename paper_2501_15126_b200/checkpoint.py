@@ -1,0 +1,58 @@
+"""Resumable long runs: the Gray range is swept as `pieces`
+power-of-two shards in order (perm_compute_shard(piece, pieces)); after each
+piece its unscaled partial (FP64 bits, or the exact INT01 T' partial) is
+appended to a JSON checkpoint.  A restart skips the recorded pieces.  The
+pieces are complete subtrees of the one-call reduction tree, so folding them
+with perm_fold reproduces perm_compute bit for bit.
+"""
+from __future__ import annotations
+
+import json
+import os
+import struct
+
+from . import perm_result
+
+
+def _key(plan, pieces: int) -> dict:
+    i = plan.info
+    return {"n": i["n"], "nnz": i["nnz"], "K": i["K"], "B": i["B"], "M": i["M"], "tasks": i["tasks"],
+            "row_perm": i["row_perm"], "col_perm": i["col_perm"], "mode": i["mode"], "pieces": pieces}
+
+
+def compute_resumable(plan, path: str, pieces: int = 256, max_pieces: int | None = None):
+    """Run (or resume) the permanent of `plan` in `pieces` shards, checkpointing
+    to `path` (JSON).  `max_pieces` bounds the pieces swept in this call (to
+    emulate an interruption).  Returns the folded perm_result when complete,
+    else None."""
+    state = {"key": _key(plan, pieces), "done": {}}
+    if os.path.exists(path):
+        with open(path) as f:
+            old = json.load(f)
+        if old.get("key") != state["key"]:
+            raise ValueError(f"checkpoint {path} belongs to another plan/geometry")
+        state = old
+    swept = 0
+    for r in range(pieces):
+        if str(r) in state["done"]:
+            continue
+        if max_pieces is not None and swept >= max_pieces:
+            return None
+        s = plan.shard(r, pieces)
+        state["done"][str(r)] = {"bits": struct.unpack("<Q", struct.pack("<d", s.value))[0],
+                                 "lo": s.exact_lo, "hi": s.exact_hi, "valid": s.exact_valid,
+                                 "sweep_ms": s.sweep_ms}
+        tmp = path + ".tmp"
+        with open(tmp, "w") as f:
+            json.dump(state, f)
+        os.replace(tmp, path)  # atomic: a crash leaves the previous checkpoint
+        swept += 1
+    shards = []
+    for r in range(pieces):
+        d = state["done"][str(r)]
+        s = perm_result()
+        s.value = struct.unpack("<d", struct.pack("<Q", d["bits"]))[0]
+        s.exact_lo, s.exact_hi, s.exact_valid = d["lo"], d["hi"], d["valid"]
+        s.sweep_ms = d["sweep_ms"]
+        shards.append(s)
+    return plan.fold(shards)

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(RT) tree_reduce_u128(const u128* __restrict__ 
 // scale 4(n mod 2) - 2 = 2(-1)^(n-1).
 __global__ void fold_f64(const double* __restrict__ part, int world, double scale, double* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double st[8];
+  double st[20];  // world <= 65536
   for (int k = 0; k < world; ++k) {
     double v = part[k];
     int lvl = 0, kk = k;

@@ -146,6 +146,7 @@ struct perm_plan_s {
   unsigned* d_counter = nullptr;
   void* d_partial = nullptr;  // 16 bytes
   void* d_scratch = nullptr;  // fold scratch (world entries)
+  size_t scratch_bytes = 0;
   void* d_tier = nullptr;     // HYBRID global tier (tier_rows x resident threads)
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   uint64_t last_first = 0, last_count = 0;
@@ -183,7 +184,8 @@ int load_device(perm_plan_s* p) {
   }
   for (auto& ev : p->ev) CUDA_TRY(cudaEventCreate(&ev));
   CUDA_TRY(cudaMalloc(&p->d_partial, 64));
-  CUDA_TRY(cudaMalloc(&p->d_scratch, 16 * 128));
+  p->scratch_bytes = 16 * 128;
+  CUDA_TRY(cudaMalloc(&p->d_scratch, p->scratch_bytes));
   CUDA_TRY(cudaMalloc(&p->d_counter, sizeof(unsigned)));
   if (!p->singular && !p->trivial1) {
     CUDA_TRY(cudaLibraryLoadData(&p->lib, p->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
@@ -242,7 +244,8 @@ int run_range(perm_plan_s* p, uint64_t first, uint64_t count, double* sweep_ms, 
 }
 
 int shard_range(perm_plan_s* p, int rank, int world, uint64_t& first, uint64_t& count) {
-  if (world < 1 || (world & (world - 1)) || world > 128) return fail(PERM_EINVAL, "world must be a power of two <= 128");
+  if (world < 1 || (world & (world - 1)) || world > 65536)
+    return fail(PERM_EINVAL, "world must be a power of two <= 65536");
   if (rank < 0 || rank >= world) return fail(PERM_EINVAL, "rank out of range");
   const uint64_t T = p->info.tasks;
   if (T >= (uint64_t)world) {
@@ -699,13 +702,13 @@ int perm_shard_range(perm_plan_t p, int rank, int world, uint64_t* first_task, u
 }
 
 double perm_fold_host(perm_plan_t p, const double* partials, int world) {
-  if (!p || !partials || p->is_u128 || world < 1 || world > 128 || (world & (world - 1))) {
-    g_err = "perm_fold_host: FP64 plan and power-of-two world <= 128 required";
+  if (!p || !partials || p->is_u128 || world < 1 || world > 65536 || (world & (world - 1))) {
+    g_err = "perm_fold_host: FP64 plan and power-of-two world <= 65536 required";
     return std::nan("");
   }
   if (p->singular) return 0.0;
   const int nn = p->trivial1 ? 1 : p->n;
-  double st[8];  // same binary-counter pairwise tree as fold_f64 (reduce.cu)
+  double st[20];  // same binary-counter pairwise tree as fold_f64 (reduce.cu)
   for (int k = 0; k < world; ++k) {
     double v = partials[k];
     int lvl = 0, kk = k;
@@ -775,7 +778,8 @@ int perm_compute_shard(perm_plan_t p, int rank, int world, perm_result* r) {
 
 int perm_fold_async(perm_plan_t p, const void* d_partials, int world, void* d_out) {
   if (!p) return fail(PERM_EINVAL, "plan is NULL");
-  if (world < 1 || world > 128 || (world & (world - 1))) return fail(PERM_EINVAL, "world must be a power of two <= 128");
+  if (world < 1 || world > 65536 || (world & (world - 1)))
+    return fail(PERM_EINVAL, "world must be a power of two <= 65536");
   CUDA_TRY(cudaSetDevice(p->device));
   const int nn = p->trivial1 ? 1 : p->n;
   CUDA_TRY(libperm_launch_fold(d_partials, world, nn, p->is_u128, p->info.K & 1, d_out, p->stream));
@@ -785,7 +789,15 @@ int perm_fold_async(perm_plan_t p, const void* d_partials, int world, void* d_ou
 int perm_fold(perm_plan_t p, const perm_result* shards, int world, perm_result* out) {
   if (!p || !shards || !out) return fail(PERM_EINVAL, "NULL argument");
   if (!p->on_device) return fail(PERM_ECUDA, "plan was created with no_device (no CPU fallback)");
-  if (world < 1 || world > 128 || (world & (world - 1))) return fail(PERM_EINVAL, "world must be a power of two <= 128");
+  if (world < 1 || world > 65536 || (world & (world - 1)))
+    return fail(PERM_EINVAL, "world must be a power of two <= 65536");
+  if ((size_t)16 * world > p->scratch_bytes) {  // grow the fold scratch
+    CUDA_TRY(cudaSetDevice(p->device));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    CUDA_TRY(cudaFree(p->d_scratch));
+    p->scratch_bytes = (size_t)16 * world;
+    CUDA_TRY(cudaMalloc(&p->d_scratch, p->scratch_bytes));
+  }
   std::vector<unsigned char> raw(16 * world, 0);
   const size_t pb = p->is_u128 ? 16 : 8;
   for (int k = 0; k < world; ++k) {

@@ -280,6 +280,25 @@ def test_hybrid_has_tier_rows_at_n36():
     check_task_partials(A, P, 3)
 
 
+def test_checkpoint_resume_bitwise(tmp_path):
+    """a run interrupted and resumed from its checkpoint folds
+    to the one-call result bit for bit (FP64 and INT01)."""
+    from paper_2501_15126_b200.checkpoint import compute_resumable
+    A = synth.erdos_renyi(32, 0.2, 5)
+    P = plan(A, mode="reg")
+    full = P.compute()
+    ck = str(tmp_path / "ck.json")
+    assert compute_resumable(P, ck, pieces=256, max_pieces=100) is None
+    assert compute_resumable(P, ck, pieces=256, max_pieces=100) is None
+    r = compute_resumable(P, ck, pieces=256)
+    assert r.value == full
+    B = synth.erdos_renyi(24, 0.25, 5, binary=True)
+    Q = plan(B, mode="int01")
+    ck2 = str(tmp_path / "ck2.json")
+    assert compute_resumable(Q, ck2, pieces=64, max_pieces=10) is None
+    assert compute_resumable(Q, ck2, pieces=64).exact() == Q.exact() == oracle.perm_nw_exact(B)
+
+
 def test_repeatable_bitwise():
     A = synth.erdos_renyi(28, 0.2, 4)
     P = plan(A)
