@@ -85,7 +85,8 @@ typedef struct {
                             work), -1 = off (plain Alg. 1 sweep), k > 0 = at most k */
   int min_blocks;        /* __launch_bounds__ min blocks per SM (register cap);
                             0 = auto from the planner's register estimate */
-  int reserved[6];
+  int zero_skip;         /* INT01 zero tracking: 0 = on, -1 = off */
+  int reserved[5];
 } perm_opts;
 
 /* Result of a computation. */

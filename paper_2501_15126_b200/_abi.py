@@ -23,7 +23,8 @@ class perm_opts(ctypes.Structure):
                 ("chunk_log2", ctypes.c_int), ("block_log2", ctypes.c_int), ("task_chunks", ctypes.c_int),
                 ("gr_ratio", ctypes.c_double), ("hybrid_c", ctypes.c_int),
                 ("threads_per_block", ctypes.c_int), ("no_device", ctypes.c_int),
-                ("factor_cols", ctypes.c_int), ("min_blocks", ctypes.c_int), ("reserved", ctypes.c_int * 6)]
+                ("factor_cols", ctypes.c_int), ("min_blocks", ctypes.c_int), ("zero_skip", ctypes.c_int),
+                ("reserved", ctypes.c_int * 5)]
 
 
 class perm_result(ctypes.Structure):

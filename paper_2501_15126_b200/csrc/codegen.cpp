@@ -174,6 +174,7 @@ struct Gen {
     cT = (S.mode == PERM_MODE_HYBRID && S.hybrid_c > 0) ? std::max(std::min(S.hybrid_c, B), std::min(U, B)) : B;
     for (int l = 0; l < B; ++l)
       if (!G[l].empty()) (l < cT ? nonempty : tier_levels).push_back(l);
+    zs = i01 && S.zero_skip && U >= 2;
     tier_slot.assign(n, -1);
     int slots = 0;
     for (int l : tier_levels)
@@ -325,10 +326,14 @@ struct Gen {
     const Factor& F = fac[f];
     if (!F.group) return pval(F.rows[0]);
     if (F.constant()) return group_value(f);  // literal a_rc
-    if (tierf(f)) return group_value(f);  // tier groups are not cached in registers
+    if (tierf(f) || zs0(f)) return group_value(f);  // tier / zero-skip level-0 groups: no register
     return reg(dv(f), pty());
   }
-  bool qreg(int l) const { return G[l].size() >= 2; }
+  // INT01 zero skip: level 0 keeps no cached registers (evaluated fresh inside
+  // the warp-uniform guard of each pair)
+  bool zs = false;
+  bool zs0(int f) const { return zs && fac[f].level == 0; }
+  bool qreg(int l) const { return G[l].size() >= 2 && !(zs && l == 0); }
   int qval(int l) { return qreg(l) ? reg("Q" + std::to_string(l), pty()) : fval(G[l][0]); }
   int next_level(int l) const {
     for (int m : nonempty)
@@ -362,7 +367,7 @@ struct Gen {
   }
   void recompute_factor(int f) {
     const Factor& F = fac[f];
-    if (!F.group || F.constant() || tierf(f)) return;
+    if (!F.group || F.constant() || tierf(f) || zs0(f)) return;
     set(dv(f), group_value(f));
   }
 
@@ -408,7 +413,49 @@ struct Gen {
   }
 
   // ---- the block body: 2^U h-steps, pairs (2k, 2k+1) -------------------------
+  // INT01 zero tracking (Sec. VI-B: "In the presence of a zero, all the
+  // expensive multiplications and the update on the result ... are skipped"):
+  // the cached product above level 0 is zero whenever a factor above level 0
+  // is zero; if that holds on all 32 lanes the pair's 128-bit work is skipped
+  // (warp-uniform branch).  The y updates always run.
+  void block_body_zero_skip() {
+    const int npairs = 1 << (U - 1);
+    for (int k = 0; k < npairs; ++k) {
+      const int u = 2 * k;
+      if (u > 0) {
+        int b = __builtin_ctz(u);
+        std::string sg = (b == U - 1) ? "sU" : (((u >> (b + 1)) & 1) ? "-" : "+");
+        flip(b, sg);
+      }
+      const bool minus = ((((u + 1) >> 1) & 1) != 0);  // static sign of the bit-0 flip (U >= 2)
+      const int ab = above(0);
+      line(std::string("if (__any_sync(0xffffffffu, ") + (ab >= 0 ? nm(ab) + " != 0" : std::string("true")) + ")) {");
+      auto save_memo = memo;
+      auto save_cur = cur;
+      auto save_leafs = leafs;
+      const std::string save_ind = ind;
+      ind += "  ";
+      std::map<int, double> shift;
+      for (int p = A.ptr[K]; p < A.ptr[K + 1]; ++p)
+        if (!dead_row(A.idx[p])) shift[A.idx[p]] = minus ? -2.0 : 2.0;
+      std::vector<int> ev, ov;
+      for (int f : G[0]) {
+        ev.push_back(node_value(fac[f].node, {}));
+        ov.push_back(node_value(fac[f].node, shift));
+      }
+      const int t = mul(sub(prod(ev), prod(ov)), ab);
+      line("cacc += " + nm(t) + ";");
+      ind = save_ind;
+      memo = save_memo;
+      cur = save_cur;
+      leafs = save_leafs;
+      line("}");
+      for (int p = A.ptr[K]; p < A.ptr[K + 1]; ++p) update(A.idx[p], A.val[p], minus ? "-" : "+");
+    }
+  }
+
   void block_body() {
+    if (zs) { block_body_zero_skip(); return; }
     std::vector<int> stack(U + 1, -1);
     const int npairs = 1 << (U - 1);
     for (int k = 0; k < npairs; ++k) {
@@ -493,7 +540,8 @@ struct Gen {
     }
     // live groups, level products, suffix chain
     for (int f = 0; f < (int)fac.size(); ++f)
-      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f)) cur[dv(f)] = group_value(f);
+      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f) && !zs0(f))
+        cur[dv(f)] = group_value(f);
     if (has_tier()) recompute_sg();
     for (int l : nonempty)
       if (qreg(l)) {
@@ -510,7 +558,7 @@ struct Gen {
       else line(std::string(VT()) + " " + xv(r) + " = " + nm(cur[xv(r)]) + ";");
     }
     for (int f = 0; f < (int)fac.size(); ++f)
-      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f))
+      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f) && !zs0(f))
         line(std::string(PT()) + " " + dv(f) + " = " + nm(cur[dv(f)]) + ";");
     if (has_tier()) line(std::string(PT()) + " SG = " + nm(cur["SG"]) + ";");
     for (int l : nonempty)

@@ -375,7 +375,9 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     const int btask = std::max(8, nb - 5 - 17);
     int B = p->opts.chunk_log2 > 0 ? p->opts.chunk_log2 : std::min(std::min(bcap, btask), std::max(0, nb - 5));
     if (B > nb) B = nb;
-    int U = p->opts.block_log2 > 0 ? p->opts.block_log2 : 5;
+    // INT01 keeps 128-bit products: a shorter unrolled block (fewer live
+    // 4-register values, faster NVRTC)
+    int U = p->opts.block_log2 > 0 ? p->opts.block_log2 : (mode == PERM_MODE_INT01 ? 3 : 5);
     if (U > B) U = B;
     const uint64_t nchunks = 1ull << (nb - B);
     const uint64_t warp_chunks = std::max<uint64_t>(1, nchunks / 32);
@@ -393,6 +395,7 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     sp.mode = mode;
     sp.threads = p->opts.threads_per_block > 0 ? p->opts.threads_per_block : 128;
     sp.nchunks_total = nchunks;
+    sp.zero_skip = mode == PERM_MODE_INT01 && p->opts.zero_skip >= 0;
     return warp_chunks / M;  // tasks
   };
 
@@ -436,7 +439,8 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
   {
     auto app = [&](const void* d, size_t nb) { pkey.append((const char*)d, nb); };
     const int hdr[] = {n, mode, (int)ord, p->opts.chunk_log2, p->opts.block_log2, p->opts.task_chunks,
-                       p->opts.factor_cols, p->opts.min_blocks, p->opts.threads_per_block};
+                       p->opts.factor_cols, p->opts.min_blocks, p->opts.threads_per_block,
+                       p->opts.hybrid_c, p->opts.zero_skip};
     app(hdr, sizeof hdr);
     app(&gr, sizeof gr);
     app(p->ccs.ptr.data(), p->ccs.ptr.size() * sizeof(int32_t));
@@ -589,8 +593,12 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
       set_hybrid(b.sp, b.o);
       if (n == 1 || p->singular) { b.ok = true; return b; }
       int stack = 0, spill = 0;
-      b.sp.min_blocks = p->opts.min_blocks > 0 ? p->opts.min_blocks
-                                               : bps_of(generate_kernel(b.o, b.xo, b.sp).est_regs + 16, b.sp.threads);
+      // start at <= 255 registers (2 blocks/SM: the FP64 pipe is already ~95 %
+      // busy there); 3 blocks only for clearly small kernels
+      b.sp.min_blocks = p->opts.min_blocks > 0
+                            ? p->opts.min_blocks
+                            : std::min(2, bps_of(generate_kernel(b.o, b.xo, b.sp).est_regs + 16, b.sp.threads));
+      if (p->opts.min_blocks <= 0 && generate_kernel(b.o, b.xo, b.sp).est_regs + 16 <= 152) b.sp.min_blocks = 3;
       for (int attempt = 0; attempt < 24; ++attempt) {
         b.kc = generate_kernel(b.o, b.xo, b.sp);
         double ms = 0;

@@ -255,7 +255,8 @@ def test_int01_factored_vs_plain(n, seed):
     A = synth.erdos_renyi(n, 0.25, seed, binary=True)
     e = oracle.perm_nw_exact(A)
     for fc in (-1, 2, 0):
-        assert plan(A, mode="int01", factor_cols=fc).exact() == e
+        for zs in (0, -1):   # zero tracking on / off
+            assert plan(A, mode="int01", factor_cols=fc, zero_skip=zs).exact() == e
 
 
 @pytest.mark.parametrize("n,p,seed", [(20, 0.3, 1), (26, 0.25, 2), (30, 0.3, 1)])

@@ -31,6 +31,9 @@ def main():
     run("C5 n=44 band depth 4", synth.givens_brickwork(44, 4, 1), mode="reg")
     run("C5' n=44 band U(0,1]", synth.band_positive(44, 4, 1), mode="reg")
     run("0/1 ER n=36 p=0.2 int01", synth.erdos_renyi(36, 0.2, 1, binary=True), mode="int01")
+    run("0/1 ER n=36 p=0.2 int01 no zero-skip", synth.erdos_renyi(36, 0.2, 1, binary=True), mode="int01",
+        zero_skip=-1)
+    run("0/1 ER n=40 p=0.2 int01", synth.erdos_renyi(40, 0.2, 1, binary=True), mode="int01")
     run("0/1 ER n=36 p=0.2 fp64", synth.erdos_renyi(36, 0.2, 1, binary=True), mode="reg")
     run("n=44 p=0.2", synth.erdos_renyi(44, 0.2, 1), mode="reg")
 
