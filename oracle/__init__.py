@@ -69,6 +69,9 @@ def _load():
             L.oracle_structural_rank.restype = ctypes.c_int
             L.oracle_structural_rank.argtypes = [ctypes.c_int, dp]
             L.oracle_max_threads.restype = ctypes.c_int
+            L.oracle_perm_naive_c.argtypes = [ctypes.c_int, dp, ldp, ldp]
+            L.oracle_nw_range_c.argtypes = [ctypes.c_int, dp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                                            ldp, ldp, ldp]
             _lib = L
     return _lib
 
@@ -182,6 +185,44 @@ def perm_band_exact(A, w: int) -> int:
     lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
     _load().oracle_perm_band_i128(A.shape[0], _ip(A), w, ctypes.byref(lo), ctypes.byref(hi))
     return _signed128(lo.value, hi.value)
+
+
+def _dense_c(A) -> np.ndarray:
+    A = np.asarray(A, dtype=np.complex128)
+    if A.ndim != 2 or A.shape[0] != A.shape[1]:
+        raise ValueError("square matrix required")
+    return np.ascontiguousarray(A).view(np.float64)   # interleaved (re, im)
+
+
+def perm_naive_complex(A) -> complex:
+    """Eq. 1 over C in complex long double."""
+    n = np.asarray(A).shape[0]
+    Ai = _dense_c(A)
+    re, im = ctypes.c_longdouble(), ctypes.c_longdouble()
+    _load().oracle_perm_naive_c(n, _dp(Ai), ctypes.byref(re), ctypes.byref(im))
+    return complex(float(re.value), float(im.value))
+
+
+def nw_range_complex(A, g_begin: int, g_end: int, threads: int = 0):
+    """Unscaled complex Alg. 1 partial over [g_begin, g_end): (sum, sum|terms|)."""
+    n = np.asarray(A).shape[0]
+    Ai = _dense_c(A)
+    re, im, sa = ctypes.c_longdouble(), ctypes.c_longdouble(), ctypes.c_longdouble()
+    _load().oracle_nw_range_c(n, _dp(Ai), g_begin, g_end, threads, ctypes.byref(re), ctypes.byref(im),
+                              ctypes.byref(sa))
+    return complex(float(re.value), float(im.value)), float(sa.value)
+
+
+def perm_nw_complex(A, threads: int = 0):
+    """perm(A) over C by Alg. 1 (+ Sec. II-A chunking), complex long double;
+    returns (perm, 2 * sum|terms|)."""
+    n = np.asarray(A).shape[0]
+    if n == 1:
+        v = complex(np.asarray(A)[0, 0])
+        return v, abs(v)
+    s, a = nw_range_complex(A, 0, 1 << (n - 1), threads)
+    f = 4 * (n % 2) - 2   # line 23
+    return s * f, 2 * a
 
 
 def structural_rank(A) -> int:

@@ -394,3 +394,101 @@ int oracle_structural_rank(int n, const double* A) {
 int oracle_max_threads(void) { return omp_get_max_threads(); }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Complex permanents (boson sampling).  Same
+// definitions as above over C: Eq. 1 and Alg. 1 in std::complex<long double>.
+// Matrices are dense row-major interleaved (re, im) pairs.
+// ---------------------------------------------------------------------------
+#include <complex>
+typedef std::complex<long double> cld;
+
+static cld naive_c_rec(int n, const cld* A, int i, uint64_t used) {
+  if (i == n) return cld(1.0L);
+  cld s(0.0L);
+  for (int c = 0; c < n; ++c) {
+    if (used >> c & 1) continue;
+    const cld a = A[(size_t)i * n + c];
+    if (a == cld(0.0L)) continue;
+    s += a * naive_c_rec(n, A, i + 1, used | (1ull << c));
+  }
+  return s;
+}
+
+// Alg. 1 lines 9-21 over a chunk of the Gray range in complex long double
+static void nw_chunk_c(int n, const std::vector<cld>& a, const std::vector<cld>& x0,
+                       const std::vector<std::vector<int>>& colrows, uint64_t gb, uint64_t ge, cld* out,
+                       long double* out_abs) {
+  cld x[64];
+  for (int i = 0; i < n; ++i) x[i] = x0[i];
+  const uint64_t G = gray(gb);
+  for (int j = 0; j + 1 < n; ++j)
+    if (G >> j & 1)
+      for (int i : colrows[j]) x[i] += a[(size_t)i * n + j];
+  cld p(0.0L);
+  long double pa = 0.0L;
+  for (uint64_t g = gb; g < ge; ++g) {
+    if (g != gb) {
+      const uint64_t d = gray(g) ^ gray(g - 1);
+      const int j = 63 - __builtin_clzll(d);
+      const long double s = 2.0L * (long double)(gray(g) >> j & 1) - 1.0L;
+      for (int i : colrows[j]) x[i] += s * a[(size_t)i * n + j];
+    }
+    cld prod(1.0L);
+    for (int i = 0; i < n; ++i) prod *= x[i];
+    if (g & 1) p -= prod; else p += prod;
+    pa += std::abs(prod);
+  }
+  *out = p;
+  *out_abs = pa;
+}
+
+extern "C" {
+
+void oracle_perm_naive_c(int n, const double* A, long double* re, long double* im) {
+  std::vector<cld> L((size_t)n * n);
+  for (size_t k = 0; k < L.size(); ++k) L[k] = cld(A[2 * k], A[2 * k + 1]);
+  const cld r = n <= 0 ? cld(1.0L) : naive_c_rec(n, L.data(), 0, 0);
+  *re = r.real();
+  *im = r.imag();
+}
+
+// Unscaled complex Alg. 1 sum over [gb, ge) (chunks of 2^12, pairwise fold)
+void oracle_nw_range_c(int n, const double* A, uint64_t gb, uint64_t ge, int threads, long double* re,
+                       long double* im, long double* sum_abs) {
+  std::vector<cld> a((size_t)n * n);
+  for (size_t k = 0; k < a.size(); ++k) a[k] = cld(A[2 * k], A[2 * k + 1]);
+  std::vector<cld> x0(n);
+  for (int i = 0; i < n; ++i) {
+    cld sum(0.0L);
+    for (int j = 0; j < n; ++j) sum += a[(size_t)i * n + j];
+    x0[i] = a[(size_t)i * n + (n - 1)] - sum / 2.0L;  // Alg. 1 lines 1-5 (reading R1)
+  }
+  std::vector<std::vector<int>> colrows(n);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i)
+      if (a[(size_t)i * n + j] != cld(0.0L)) colrows[j].push_back(i);
+  const uint64_t CH = 1ull << ORACLE_CHUNK_LOG2;
+  const uint64_t len = ge > gb ? ge - gb : 0, nch = (len + CH - 1) / CH;
+  std::vector<cld> part(nch);
+  std::vector<long double> pabs(nch);
+  const int nt = threads > 0 ? threads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nt)
+  for (long long c = 0; c < (long long)nch; ++c) {
+    const uint64_t s0 = gb + (uint64_t)c * CH, s1 = std::min(ge, s0 + CH);
+    nw_chunk_c(n, a, x0, colrows, s0, s1, &part[c], &pabs[c]);
+  }
+  // pairwise fold in chunk order
+  for (uint64_t h = 1; h < nch; h <<= 1)
+    for (uint64_t i = 0; i + h < nch; i += 2 * h) { part[i] += part[i + h]; pabs[i] += pabs[i + h]; }
+  const cld r = nch ? part[0] : cld(0.0L);
+  *re = r.real();
+  *im = r.imag();
+  *sum_abs = nch ? pabs[0] : 0.0L;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+}  // extern "C"

@@ -113,6 +113,41 @@ def band_positive(n: int, depth: int, seed: int) -> np.ndarray:
     return A
 
 
+def erdos_renyi_complex(n: int, p: float, seed: int, max_attempts: int = 1000) -> np.ndarray:
+    """ER pattern as erdos_renyi; value r e^{i theta}, r in (0,1], theta = 2 pi u."""
+    rng = SplitMix64(seed ^ 0xC0FFEE)
+    for _ in range(max_attempts):
+        A = np.zeros((n, n), dtype=np.complex128)
+        for i in range(n):
+            for j in range(n):
+                if rng.uniform() < p:
+                    r = rng.unit_open0()
+                    th = 2.0 * math.pi * rng.uniform()
+                    A[i, j] = r * complex(math.cos(th), math.sin(th))
+        if _has_perfect_matching(A != 0):
+            return A
+    raise RuntimeError("no structurally nonsingular complex ER draw")
+
+
+def unitary_brickwork(n: int, depth: int, seed: int) -> np.ndarray:
+    """Complex unitary of `depth` brickwork layers of beam splitters
+    [[e^{i phi} cos t, -sin t], [e^{i phi} sin t, cos t]] on neighbouring modes
+    (low-depth boson sampling interferometer); half-width <= depth."""
+    rng = SplitMix64(seed ^ 0xB05)
+    U = np.eye(n, dtype=np.complex128)
+    for layer in range(depth):
+        L = np.eye(n, dtype=np.complex128)
+        for a in range(layer % 2, n - 1, 2):
+            t = 2.0 * math.pi * rng.uniform()
+            ph = 2.0 * math.pi * rng.uniform()
+            e = complex(math.cos(ph), math.sin(ph))
+            L[a, a], L[a, a + 1] = e * math.cos(t), -math.sin(t)
+            L[a + 1, a], L[a + 1, a + 1] = e * math.sin(t), math.cos(t)
+        U = L @ U
+    U[np.abs(U) < 1e-300] = 0.0
+    return U
+
+
 def half_bandwidth(A: np.ndarray) -> int:
     ii, jj = np.nonzero(A)
     return int(np.max(np.abs(ii - jj))) if ii.size else 0

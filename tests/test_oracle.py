@@ -291,3 +291,64 @@ def test_structural_rank_cases():
     for _ in range(6):
         A = (rng.uniform(size=(5, 5)) < 0.3).astype(float)
         assert oracle.structural_rank(A) == brute_rank(A)
+
+
+# ---- complex permanents --------------------------------------
+
+def brute_perm_c(A):
+    n = A.shape[0]
+    return sum(math.prod(A[i, s[i]] for i in range(n)) for s in itertools.permutations(range(n)))
+
+
+def test_complex_2x2_and_diagonal():
+    A = np.array([[1 + 2j, 3 - 1j], [0.5j, 2 + 0j]])
+    exp = A[0, 0] * A[1, 1] + A[0, 1] * A[1, 0]
+    assert abs(oracle.perm_naive_complex(A) - exp) < 1e-15
+    assert abs(oracle.perm_nw_complex(A)[0] - exp) < 1e-14
+    D = np.diag([1 + 1j, 2 - 0.5j, -1j, 0.25 + 3j, 1.5])
+    assert abs(oracle.perm_nw_complex(D)[0] - np.prod(np.diag(D))) < 1e-13
+
+
+@pytest.mark.parametrize("n", [3, 6, 9])
+def test_complex_scaled_ones(n):
+    z = 0.7 - 0.4j
+    exp = math.factorial(n) * z ** n
+    assert abs(oracle.perm_naive_complex(z * np.ones((n, n))) - exp) <= 1e-14 * abs(exp)
+    assert abs(oracle.perm_nw_complex(z * np.ones((n, n)))[0] - exp) <= 1e-13 * abs(exp)
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_complex_naive_vs_brute_and_nw(seed):
+    n = 4 + seed % 4
+    A = synth.erdos_renyi_complex(n, 0.5, seed)
+    b = brute_perm_c(A)
+    v, sabs = oracle.perm_nw_complex(A)
+    assert abs(oracle.perm_naive_complex(A) - b) <= 1e-14 * max(abs(b), 1e-300) + 1e-300
+    assert abs(v - b) <= 1e-15 * sabs
+    # conjugation and real-part consistency
+    assert abs(oracle.perm_naive_complex(A.conj()) - b.conjugate()) <= 1e-14 * max(abs(b), 1e-300)
+    R = np.abs(A)
+    assert abs(oracle.perm_nw_complex(R)[0] - oracle.perm_nw(R)[0]) <= 1e-13 * abs(oracle.perm_nw(R)[0])
+
+
+def test_complex_unitary_brickwork_vs_band_structure():
+    U = synth.unitary_brickwork(10, 3, 1)
+    assert np.allclose(U.conj().T @ U, np.eye(10))
+    assert synth.half_bandwidth(U) <= 3
+    v, sabs = oracle.perm_nw_complex(U)
+    assert abs(v - oracle.perm_naive_complex(U)) <= 1e-14 * sabs
+    rng = np.random.default_rng(3)
+    P, Q = rng.permutation(10), rng.permutation(10)
+    assert abs(oracle.perm_nw_complex(U[np.ix_(P, Q)])[0] - v) <= 1e-14 * sabs
+
+
+def test_complex_block_diagonal_product():
+    rng = np.random.default_rng(5)
+    B1 = rng.normal(size=(3, 3)) + 1j * rng.normal(size=(3, 3))
+    B2 = rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4))
+    A = np.zeros((7, 7), dtype=complex)
+    A[:3, :3] = B1
+    A[3:, 3:] = B2
+    exp = brute_perm_c(B1) * brute_perm_c(B2)
+    v, sabs = oracle.perm_nw_complex(A)
+    assert abs(v - exp) <= 1e-14 * sabs
