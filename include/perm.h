@@ -63,7 +63,9 @@ typedef enum {
   PERM_MODE_REG = 1,    /* FP64, x of every in-chunk row in registers (Sec. III) */
   PERM_MODE_HYBRID = 2, /* FP64, rows first flipped by columns >= c (Alg. 4) live in a
                            per-thread memory tier (Sec. V; B200: shared memory) */
-  PERM_MODE_INT01 = 3   /* exact: 2x in int32, products/sums mod 2^128 (0/1 inputs) */
+  PERM_MODE_INT01 = 3,  /* exact: 2x in int32, products/sums mod 2^128 (0/1 inputs) */
+  PERM_MODE_COMPLEX = 4 /* reported by perm_plan_get_info for perm_plan_complex plans
+                           (complex FP64 sweep; not a valid request mode) */
 } perm_mode;
 
 /* Options; a zero-initialised struct means "all defaults". */
@@ -99,6 +101,7 @@ typedef struct {
   uint64_t products;     /* product terms evaluated (2^(n-1) for a full run) */
   double sweep_ms;       /* device time of the sweep kernel (CUDA events) */
   double reduce_ms;      /* device time of the deterministic reduction */
+  double value_im;       /* complex plans: imaginary part of `value` (else 0) */
 } perm_result;
 
 /* Plan inspection (all indices refer to the ORDERED matrix unless noted). */
@@ -146,6 +149,15 @@ int perm_plan(int n, perm_format fmt, const int32_t *ptr, const int32_t *idx,
 int perm_plan_ex(int n, perm_format fmt, const int32_t *ptr, const int32_t *idx,
                  const double *val, perm_ordering ord, const perm_opts *opts,
                  perm_plan_t *out);
+
+/* Complex matrices (boson-sampling unitaries): as perm_plan_ex
+ * but val_re_im holds 2*nnz doubles, (re, im) per nonzero in idx order; a
+ * nonzero is any pair other than (0, 0).  Modes AUTO/REG (complex FP64 sweep,
+ * info.mode = PERM_MODE_COMPLEX); results carry value + i*value_im; partials
+ * are 16 bytes (re, im). */
+int perm_plan_complex(int n, perm_format fmt, const int32_t *ptr, const int32_t *idx,
+                      const double *val_re_im, perm_ordering ord, const perm_opts *opts,
+                      perm_plan_t *out);
 
 /* perm(A) on one GPU (whole Gray range).  NaN on error (see perm_last_error).
  * Synchronises the plan's stream. */

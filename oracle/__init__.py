@@ -70,6 +70,7 @@ def _load():
             L.oracle_structural_rank.argtypes = [ctypes.c_int, dp]
             L.oracle_max_threads.restype = ctypes.c_int
             L.oracle_perm_naive_c.argtypes = [ctypes.c_int, dp, ldp, ldp]
+            L.oracle_perm_band_c.argtypes = [ctypes.c_int, dp, ctypes.c_int, ldp, ldp]
             L.oracle_nw_range_c.argtypes = [ctypes.c_int, dp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
                                             ldp, ldp, ldp]
             _lib = L
@@ -200,6 +201,15 @@ def perm_naive_complex(A) -> complex:
     Ai = _dense_c(A)
     re, im = ctypes.c_longdouble(), ctypes.c_longdouble()
     _load().oracle_perm_naive_c(n, _dp(Ai), ctypes.byref(re), ctypes.byref(im))
+    return complex(float(re.value), float(im.value))
+
+
+def perm_band_complex(A, w: int) -> complex:
+    """Band DP of Eq. 1 over C (a_ij = 0 for |i - j| > w)."""
+    n = np.asarray(A).shape[0]
+    Ai = _dense_c(A)
+    re, im = ctypes.c_longdouble(), ctypes.c_longdouble()
+    _load().oracle_perm_band_c(n, _dp(Ai), w, ctypes.byref(re), ctypes.byref(im))
     return complex(float(re.value), float(im.value))
 
 

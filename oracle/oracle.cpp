@@ -453,6 +453,16 @@ void oracle_perm_naive_c(int n, const double* A, long double* re, long double* i
   *im = r.imag();
 }
 
+// band DP of Eq. 1 over C (same textbook DP as oracle_perm_band_ld)
+void oracle_perm_band_c(int n, const double* A, int w, long double* re, long double* im) {
+  const cld r = band_dp<cld>(n, w, [&](int i, int j) {
+    const size_t k = (size_t)i * n + j;
+    return cld(A[2 * k], A[2 * k + 1]);
+  });
+  *re = r.real();
+  *im = r.imag();
+}
+
 // Unscaled complex Alg. 1 sum over [gb, ge) (chunks of 2^12, pairwise fold)
 void oracle_nw_range_c(int n, const double* A, uint64_t gb, uint64_t ge, int threads, long double* re,
                        long double* im, long double* sum_abs) {

@@ -46,8 +46,10 @@ def _f64(a):
 
 
 def dense_to_ccs(A):
-    """Dense -> (cptrs, rids, cvals) (Sec. II, P:51-57)."""
-    A = np.asarray(A, dtype=np.float64)
+    """Dense -> (cptrs, rids, cvals) (Sec. II); complex dense -> complex cvals."""
+    A = np.asarray(A)
+    cpx = np.iscomplexobj(A)
+    A = A.astype(np.complex128 if cpx else np.float64)
     n = A.shape[0]
     ptr, idx, val = [0], [], []
     for j in range(n):
@@ -55,11 +57,11 @@ def dense_to_ccs(A):
         idx.extend(rows.tolist())
         val.extend(A[rows, j].tolist())
         ptr.append(len(idx))
-    return np.array(ptr, np.int32), np.array(idx, np.int32), np.array(val, np.float64)
+    return np.array(ptr, np.int32), np.array(idx, np.int32), np.array(val, np.complex128 if cpx else np.float64)
 
 
 def dense_to_crs(A):
-    return dense_to_ccs(np.asarray(A, dtype=np.float64).T)
+    return dense_to_ccs(np.asarray(A).T)
 
 
 def make_opts(mode="auto", device=0, stream=None, chunk_log2=0, block_log2=0, task_chunks=0,
@@ -86,9 +88,15 @@ def perm_plan(n, fmt, ptr, idx, val, ordering="auto", opts: perm_opts | None = N
     L = _abi.lib()
     ptr_a, p_ptr = _i32(ptr)
     idx_a, p_idx = _i32(idx)
-    val_a, p_val = _f64(val)
     h = ctypes.c_void_p()
     o = ORDER[ordering] if isinstance(ordering, str) else int(ordering)
+    if np.iscomplexobj(val):   # complex permanent: interleaved (re, im)
+        val_a, p_val = _f64(np.ascontiguousarray(np.asarray(val, np.complex128)).view(np.float64))
+        st = L.perm_plan_complex(n, fmt, p_ptr, p_idx, p_val, o, ctypes.byref(opts or make_opts()),
+                                 ctypes.byref(h))
+        _check(st, "perm_plan_complex")
+        return h.value
+    val_a, p_val = _f64(val)
     if opts is None:
         st = L.perm_plan(n, fmt, p_ptr, p_idx, p_val, o, ctypes.byref(h))
     else:
@@ -184,16 +192,19 @@ class Plan:
 
     def __init__(self, n, fmt, ptr, idx, val, ordering="auto", **opts):
         self.n = int(n)
+        self.is_complex = bool(np.iscomplexobj(val))
         self.handle = perm_plan(self.n, fmt, ptr, idx, val, ordering, make_opts(**opts))
 
     @classmethod
     def from_dense(cls, A, ordering="auto", fmt=PERM_CCS, **opts):
-        A = np.asarray(A, dtype=np.float64)
+        A = np.asarray(A)
+        A = A.astype(np.complex128 if np.iscomplexobj(A) else np.float64)
         ptr, idx, val = dense_to_ccs(A) if fmt == PERM_CCS else dense_to_crs(A)
         return cls(A.shape[0], fmt, ptr, idx, val, ordering, **opts)
 
-    def compute(self) -> float:
-        return self.compute_ex().value
+    def compute(self):
+        r = self.compute_ex()
+        return r.complex_value() if self.is_complex else r.value
 
     def compute_ex(self) -> perm_result:
         return perm_compute_ex(self.handle)

@@ -30,7 +30,11 @@ class perm_opts(ctypes.Structure):
 class perm_result(ctypes.Structure):
     _fields_ = [("value", ctypes.c_double), ("exact_lo", ctypes.c_uint64), ("exact_hi", ctypes.c_uint64),
                 ("exact_valid", ctypes.c_int), ("world", ctypes.c_int), ("rank", ctypes.c_int),
-                ("products", ctypes.c_uint64), ("sweep_ms", ctypes.c_double), ("reduce_ms", ctypes.c_double)]
+                ("products", ctypes.c_uint64), ("sweep_ms", ctypes.c_double), ("reduce_ms", ctypes.c_double),
+                ("value_im", ctypes.c_double)]
+
+    def complex_value(self) -> complex:
+        return complex(self.value, self.value_im)
 
     def exact(self):
         if not self.exact_valid:
@@ -65,7 +69,8 @@ EXPORTS = ["perm_plan", "perm_plan_ex", "perm_compute", "perm_compute_ex", "perm
            "perm_compute_shard_async", "perm_fold", "perm_fold_async", "perm_partial_bytes",
            "perm_debug_task_partials", "perm_last_timing", "perm_plan_get_info", "perm_plan_source", "perm_plan_cubin",
            "perm_free", "perm_last_error", "perm_version", "perm_structural_rank", "perm_order",
-           "perm_partition", "perm_alg2_launch_parameters", "perm_shard_range", "perm_fold_host"]
+           "perm_partition", "perm_alg2_launch_parameters", "perm_shard_range", "perm_fold_host",
+           "perm_plan_complex"]
 
 _lib = None
 
@@ -84,6 +89,8 @@ def lib():
     L.perm_plan.argtypes = [ctypes.c_int, ctypes.c_int, i32p, i32p, dp, ctypes.c_int, ctypes.POINTER(P)]
     L.perm_plan_ex.argtypes = [ctypes.c_int, ctypes.c_int, i32p, i32p, dp, ctypes.c_int,
                                ctypes.POINTER(perm_opts), ctypes.POINTER(P)]
+    L.perm_plan_complex.argtypes = [ctypes.c_int, ctypes.c_int, i32p, i32p, dp, ctypes.c_int,
+                                    ctypes.POINTER(perm_opts), ctypes.POINTER(P)]
     L.perm_compute.restype = ctypes.c_double
     L.perm_compute.argtypes = [P]
     L.perm_compute_ex.argtypes = [P, ctypes.POINTER(perm_result)]

@@ -48,6 +48,7 @@
 #include <map>
 #include <set>
 #include <sstream>
+#include <complex>
 #include <tuple>
 
 #include "perm_internal.h"
@@ -101,7 +102,14 @@ struct Gen {
   std::string ind = "";
 
   // ---- value numbering (SSA within one straight-line region) ----------------
-  struct Val { char op; int a, b, c; char ty; std::string name; };
+  struct Val {
+    char op;
+    int a, b, c;
+    char ty;
+    std::string name;
+    bool real_lit = false;  // complex literal with zero imaginary part
+    double re = 0;          // its real part
+  };
   std::vector<Val> vals;
   std::map<std::tuple<char, int, int, int>, int> memo;
   std::map<std::string, int> leafs;      // leaf text -> id (literals, region-start registers)
@@ -110,13 +118,16 @@ struct Gen {
   int tmp = 0;
 
   std::vector<Node> nodes;
-  std::vector<std::map<int, double>> colval;  // ordered column -> (row -> a)
+  typedef std::complex<double> zd;
+  std::vector<std::map<int, zd>> colval;  // ordered column -> (row -> a) (imag 0 for real)
+  bool cx = false;                        // complex FP64 sweep
 
   Gen(const Csx& a, const std::vector<double>& x, const KernelSpec& s)
       : A(a), S(s), x0(x), i01(s.mode == PERM_MODE_INT01), n(a.n), K(s.K), B(s.B), U(s.U) {
+    cx = S.mode == PERM_MODE_COMPLEX_INTERNAL;
     colval.assign(n, {});
     for (int j = 0; j < n; ++j)
-      for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) colval[j][A.idx[p]] = A.val[p];
+      for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) colval[j][A.idx[p]] = zd(A.val[p], A.im(p));
     // replay the elimination of ordered columns 0..K-1
     std::vector<int> root_of(n);          // row -> current root node
     for (int r = 0; r < n; ++r) {
@@ -187,11 +198,14 @@ struct Gen {
   bool has_tier() const { return !tier_levels.empty(); }
   bool tierf(int f) const { return fac[f].level >= cT; }
 
-  const char* PT() const { return i01 ? "u128" : "double"; }
-  const char* VT() const { return i01 ? "int" : "double"; }
-  const char* tyname(char t) const { return t == 'i' ? "int" : (t == 'u' ? "u128" : "double"); }
-  char pty() const { return i01 ? 'u' : 'd'; }
-  char xty() const { return i01 ? 'i' : 'd'; }
+  const char* PT() const { return i01 ? "u128" : (cx ? "cplx" : "double"); }
+  const char* VT() const { return i01 ? "int" : (cx ? "cplx" : "double"); }
+  const char* tyname(char t) const {
+    return t == 'i' ? "int" : (t == 'u' ? "u128" : (t == 'z' ? "cplx" : "double"));
+  }
+  char pty() const { return i01 ? 'u' : (cx ? 'z' : 'd'); }
+  char xty() const { return i01 ? 'i' : (cx ? 'z' : 'd'); }
+  std::string zero() const { return cx ? "cplx{0.0, 0.0}" : "0"; }
   std::string xv(int r) const { return "x" + std::to_string(r); }
   std::string dv(int f) const { return "D" + std::to_string(fac[f].col); }
   std::vector<char> dead;
@@ -207,6 +221,12 @@ struct Gen {
     return leafs[text] = (int)vals.size() - 1;
   }
   int lit(double v) { return leaf(hexlit(v), 'd'); }
+  int zlit(zd v) {
+    const int id = leaf("cplx{" + hexlit(v.real()) + ", " + hexlit(v.imag()) + "}", 'z');
+    if (v.imag() == 0.0) { vals[id].real_lit = true; vals[id].re = v.real(); }
+    return id;
+  }
+  int vlit(zd v) { return cx ? zlit(v) : lit(v.real()); }  // value literal of the sweep's type
   int ilit(long long v) { return leaf(std::to_string(v), 'i'); }
   int ulit(long long v) { return leaf("((u128)" + std::to_string(v) + ")", 'u'); }
   const std::string& nm(int id) const { return vals[id].name; }
@@ -225,16 +245,54 @@ struct Gen {
     auto it = memo.find(key);
     if (it != memo.end()) return it->second;
     char ty = vals[a].ty;
+    const bool z = vals[a].ty == 'z' || (b >= 0 && vals[b].ty == 'z') || (c >= 0 && vals[c].ty == 'z');
     std::string expr;
-    switch (op) {
-      case '+': expr = nm(a) + " + " + nm(b); break;
-      case '-': expr = nm(a) + " - " + nm(b); break;
-      case '*': expr = nm(a) + " * " + nm(b); break;
-      case 'f': expr = "fma(" + nm(a) + ", " + nm(b) + ", " + nm(c) + ")"; break;
-      case 'c': expr = "(u128)(i128)" + nm(a); ty = 'u'; break;
-      case 'h': expr = "2 * " + nm(a); break;  // int doubling (INT01)
+    double w = 1;  // executed DP instructions
+    if (z) {  // complex: cplx helpers of the generated prelude (1, 2 or 4 DP instructions)
+      ty = 'z';
+      // a literal with zero imaginary part multiplies / adds as a real number
+      auto rl = [&](int v) { return vals[v].real_lit; };
+      auto rs = [&](int v) { return hexlit(vals[v].re); };
+      switch (op) {
+        case '+':
+          if (rl(b)) { expr = "caddr(" + nm(a) + ", " + rs(b) + ")"; w = 1; }
+          else if (rl(a)) { expr = "caddr(" + nm(b) + ", " + rs(a) + ")"; w = 1; }
+          else { expr = "cadd(" + nm(a) + ", " + nm(b) + ")"; w = 2; }
+          break;
+        case '-':
+          if (rl(b)) { expr = "caddr(" + nm(a) + ", -" + rs(b) + ")"; w = 1; }
+          else { expr = "csub(" + nm(a) + ", " + nm(b) + ")"; w = 2; }
+          break;
+        case '*':
+          if (vals[a].ty == 'd') { expr = "cscale(" + nm(a) + ", " + nm(b) + ")"; w = 2; }
+          else if (vals[b].ty == 'd') { expr = "cscale(" + nm(b) + ", " + nm(a) + ")"; w = 2; }
+          else if (rl(a)) { expr = "cscale(" + rs(a) + ", " + nm(b) + ")"; w = 2; }
+          else if (rl(b)) { expr = "cscale(" + rs(b) + ", " + nm(a) + ")"; w = 2; }
+          else { expr = "cmul(" + nm(a) + ", " + nm(b) + ")"; w = 4; }
+          break;
+        case 'f':
+          if (vals[a].ty == 'd' && rl(b)) {  // s * (real a) + x: only the real part moves
+            expr = "cfmar(" + nm(a) + ", " + rs(b) + ", " + nm(c) + ")"; w = 1;
+          } else if (vals[a].ty == 'd') {
+            expr = "cfma_s(" + nm(a) + ", " + nm(b) + ", " + nm(c) + ")"; w = 2;
+          } else if (rl(a)) {
+            expr = "cfma_s(" + rs(a) + ", " + nm(b) + ", " + nm(c) + ")"; w = 2;
+          } else {
+            expr = "cfma(" + nm(a) + ", " + nm(b) + ", " + nm(c) + ")"; w = 4;
+          }
+          break;
+      }
+    } else {
+      switch (op) {
+        case '+': expr = nm(a) + " + " + nm(b); break;
+        case '-': expr = nm(a) + " - " + nm(b); break;
+        case '*': expr = nm(a) + " * " + nm(b); break;
+        case 'f': expr = "fma(" + nm(a) + ", " + nm(b) + ", " + nm(c) + ")"; break;
+        case 'c': expr = "(u128)(i128)" + nm(a); ty = 'u'; w = 0; break;
+        case 'h': expr = "2 * " + nm(a); break;  // int doubling (INT01)
+      }
     }
-    if (op != 'c') ops += 1;
+    ops += w;
     std::string name = "t" + std::to_string(tmp++);
     line(std::string("const ") + tyname(ty) + " " + name + " = " + expr + ";");
     vals.push_back({op, a, b, c, ty, name});
@@ -290,30 +348,30 @@ struct Gen {
   int pval(int r) { return i01 ? mk('c', xval(r), -1) : xval(r); }  // row value as product type
   // value of elimination-tree node `id` with row shifts `sh` (ancestors'
   // eliminated columns switched in; INT01 shifts in doubled units)
-  int node_value(int id, const std::map<int, double>& sh) {
+  int node_value(int id, const std::map<int, zd>& sh) {
     const Node& N = nodes[id];
-    auto shift = [&](int r) { auto it = sh.find(r); return it == sh.end() ? 0.0 : it->second; };
+    auto shift = [&](int r) { auto it = sh.find(r); return it == sh.end() ? zd(0.0) : it->second; };
     if (N.leaf) {
-      const double s = shift(N.row);
-      if (i01) return s == 0 ? pval(N.row) : mk('c', add(xval(N.row), ilit(std::llround(s))), -1);
-      return s == 0 ? xval(N.row) : add(xval(N.row), lit(s));
+      const zd s = shift(N.row);
+      if (i01) return s == zd(0.0) ? pval(N.row) : mk('c', add(xval(N.row), ilit(std::llround(s.real()))), -1);
+      return s == zd(0.0) ? xval(N.row) : add(xval(N.row), vlit(s));
     }
-    const std::map<int, double>& cv = colval[N.col];
+    const std::map<int, zd>& cv = colval[N.col];
     if (N.ch.size() == 1 && nodes[N.ch[0]].leaf)  // (y + s + a) - (y + s) = a exactly
-      return i01 ? ulit(2) : lit(cv.at(nodes[N.ch[0]].row));
+      return i01 ? ulit(2) : vlit(cv.at(nodes[N.ch[0]].row));
     if (N.ch.size() == 2 && nodes[N.ch[0]].leaf && nodes[N.ch[1]].leaf) {
       const int r1 = nodes[N.ch[0]].row, r2 = nodes[N.ch[1]].row;
-      const double s1 = shift(r1), s2 = shift(r2);
+      const zd s1 = shift(r1), s2 = shift(r2);
       if (i01) {  // (x1+s1+2)(x2+s2+2) - (x1+s1)(x2+s2) = 2 (x1 + x2) + (2 s1 + 2 s2 + 4)
         int t = mk('h', add(xval(r1), xval(r2)), -1);
-        return mk('c', add(t, ilit(std::llround(2 * s1 + 2 * s2 + 4))), -1);
+        return mk('c', add(t, ilit(std::llround(2 * s1.real() + 2 * s2.real() + 4))), -1);
       }
       // a1 (y2 + s2) + a2 (y1 + s1) + a1 a2: two FMAs, no cancellation
-      const double a1 = cv.at(r1), a2 = cv.at(r2);
-      return mk('f', lit(a1), xval(r2), mk('f', lit(a2), xval(r1), lit(a1 * a2 + a1 * s2 + a2 * s1)));
+      const zd a1 = cv.at(r1), a2 = cv.at(r2);
+      return mk('f', vlit(a1), xval(r2), mk('f', vlit(a2), xval(r1), vlit(a1 * a2 + a1 * s2 + a2 * s1)));
     }
-    std::map<int, double> shin = sh;
-    for (auto& kv : cv) shin[kv.first] += i01 ? 2.0 : kv.second;
+    std::map<int, zd> shin = sh;
+    for (auto& kv : cv) shin[kv.first] += i01 ? zd(2.0) : kv.second;
     std::vector<int> in, out;
     for (int c : N.ch) {
       in.push_back(node_value(c, shin));
@@ -329,11 +387,9 @@ struct Gen {
     if (tierf(f) || zs0(f)) return group_value(f);  // tier / zero-skip level-0 groups: no register
     return reg(dv(f), pty());
   }
-  // INT01 zero skip: level 0 keeps no cached registers (evaluated fresh inside
-  // the warp-uniform guard of each pair)
-  bool zs = false;
-  bool zs0(int f) const { return zs && fac[f].level == 0; }
-  bool qreg(int l) const { return G[l].size() >= 2 && !(zs && l == 0); }
+  bool zs = false;  // INT01 block-level zero skip (block_zero_skip_body)
+  bool zs0(int) const { return false; }
+  bool qreg(int l) const { return G[l].size() >= 2; }
   int qval(int l) { return qreg(l) ? reg("Q" + std::to_string(l), pty()) : fval(G[l][0]); }
   int next_level(int l) const {
     for (int m : nonempty)
@@ -372,17 +428,18 @@ struct Gen {
   }
 
   // one update y_r +-= a_rj.  sign: "+", "-" (static) or a runtime +-1 register
-  void update(int r, double a, const std::string& sign) {
+  void update(int r, int pos, const std::string& sign) {  // pos: CCS position of a_rj
     if (dead_row(r)) return;  // only enters through the constant D_k = a_rk
+    const zd a(A.val[pos], A.im(pos));
     int x = xval(r), y;
     if (i01) {
       if (sign == "+") y = add(x, ilit(2));
       else if (sign == "-") y = sub(x, ilit(2));
       else y = add(x, reg(sign, 'i'));  // runtime sign register holds +-2
     } else {
-      if (sign == "+") y = add(x, lit(a));
-      else if (sign == "-") y = sub(x, lit(a));
-      else y = mk('f', reg(sign, 'd'), lit(a), x);
+      if (sign == "+") y = add(x, vlit(a));
+      else if (sign == "-") y = sub(x, vlit(a));
+      else y = mk('f', reg(sign, 'd'), vlit(a), x);
     }
     set(xv(r), y);
   }
@@ -392,7 +449,7 @@ struct Gen {
     const int j = K + b;
     std::set<int> facs, levels;
     for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) {
-      update(A.idx[p], A.val[p], sign);
+      update(A.idx[p], p, sign);
       facs.insert(fac_of_row[A.idx[p]]);
     }
     for (int f : facs) recompute_factor(f);
@@ -414,48 +471,49 @@ struct Gen {
 
   // ---- the block body: 2^U h-steps, pairs (2k, 2k+1) -------------------------
   // INT01 zero tracking (Sec. VI-B: "In the presence of a zero, all the
-  // expensive multiplications and the update on the result ... are skipped"):
-  // the cached product above level 0 is zero whenever a factor above level 0
-  // is zero; if that holds on all 32 lanes the pair's 128-bit work is skipped
-  // (warp-uniform branch).  The y updates always run.
-  void block_body_zero_skip() {
-    const int npairs = 1 << (U - 1);
-    for (int k = 0; k < npairs; ++k) {
-      const int u = 2 * k;
-      if (u > 0) {
-        int b = __builtin_ctz(u);
-        std::string sg = (b == U - 1) ? "sU" : (((u >> (b + 1)) & 1) ? "-" : "+");
-        flip(b, sg);
-      }
-      const bool minus = ((((u + 1) >> 1) & 1) != 0);  // static sign of the bit-0 flip (U >= 2)
-      const int ab = above(0);
-      line(std::string("if (__any_sync(0xffffffffu, ") + (ab >= 0 ? nm(ab) + " != 0" : std::string("true")) + ")) {");
-      auto save_memo = memo;
-      auto save_cur = cur;
-      auto save_leafs = leafs;
-      const std::string save_ind = ind;
-      ind += "  ";
-      std::map<int, double> shift;
-      for (int p = A.ptr[K]; p < A.ptr[K + 1]; ++p)
-        if (!dead_row(A.idx[p])) shift[A.idx[p]] = minus ? -2.0 : 2.0;
-      std::vector<int> ev, ov;
-      for (int f : G[0]) {
-        ev.push_back(node_value(fac[f].node, {}));
-        ov.push_back(node_value(fac[f].node, shift));
-      }
-      const int t = mul(sub(prod(ev), prod(ov)), ab);
-      line("cacc += " + nm(t) + ";");
-      ind = save_ind;
-      memo = save_memo;
-      cur = save_cur;
-      leafs = save_leafs;
-      line("}");
-      for (int p = A.ptr[K]; p < A.ptr[K + 1]; ++p) update(A.idx[p], A.val[p], minus ? "-" : "+");
+  // expensive multiplications and the update on the result ... are skipped"),
+  // at block granularity: every term of the block carries the cached product
+  // of the factors above the in-block levels (S_U); when it is zero on all 32
+  // lanes (warp vote) the block contributes 0 and is replaced by its net
+  // effect on y -- over a full reflected Gray block only column U-1 changes
+  // state (the lower columns flip an even number of times with alternating
+  // signs; exact in integers).  An executed block first refreshes the in-block
+  // levels (they may be stale after skipped blocks).
+  void block_zero_skip_body() {
+    const int su = above(U - 1);
+    if (su < 0) { block_body(); return; }
+    line("if (__any_sync(0xffffffffu, " + nm(su) + " != 0)) {");
+    auto save_memo = memo;
+    auto save_cur = cur;
+    auto save_leafs = leafs;
+    const std::string save_ind = ind;
+    ind += "  ";
+    // refresh levels < U from y: groups, level products, suffix chain
+    for (int l : nonempty) {
+      if (l >= U) continue;
+      for (int f : G[l]) recompute_factor(f);
+      recompute_q(l);
     }
+    for (auto it = nonempty.rbegin(); it != nonempty.rend(); ++it)
+      if (*it >= 1 && *it < U) recompute_s(*it);
+    block_body();
+    end_region();
+    ind = save_ind;
+    memo = save_memo;
+    cur = save_cur;
+    leafs = save_leafs;
+    line("} else {");
+    ind += "  ";
+    for (int p = A.ptr[K + U - 1]; p < A.ptr[K + U]; ++p) update(A.idx[p], p, "sU");
+    end_region();
+    ind = save_ind;
+    memo = save_memo;
+    cur = save_cur;
+    leafs = save_leafs;
+    line("}");
   }
 
   void block_body() {
-    if (zs) { block_body_zero_skip(); return; }
     std::vector<int> stack(U + 1, -1);
     const int npairs = 1 << (U - 1);
     for (int k = 0; k < npairs; ++k) {
@@ -472,7 +530,7 @@ struct Gen {
         const int j = K;
         std::set<int> facs;
         for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) {
-          update(A.idx[p], A.val[p], sg0);
+          update(A.idx[p], p, sg0);
           facs.insert(fac_of_row[A.idx[p]]);
         }
         for (int f : facs) recompute_factor(f);
@@ -508,7 +566,8 @@ struct Gen {
     begin_region();
     for (int r = 0; r < n; ++r) {
       if (dead_row(r)) continue;
-      cur[xv(r)] = i01 ? ilit(std::llround(x0[r])) : lit(x0[r]);
+      // x0 per row; complex sweeps pass (re, im) pairs
+      cur[xv(r)] = i01 ? ilit(std::llround(x0[r])) : (cx ? zlit(zd(x0[2 * r], x0[2 * r + 1])) : lit(x0[r]));
     }
     for (int b = std::max(B - 1, 0); b < nbits; ++b) {
       const int j = K + b;
@@ -525,7 +584,7 @@ struct Gen {
              ") & 1ull) * 0x3FF0000000000000ull));");
         for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p)
           if (!dead_row(A.idx[p]))
-            set(xv(A.idx[p]), mk('f', leaf(bn, 'd'), lit(A.val[p]), xval(A.idx[p])));
+            set(xv(A.idx[p]), mk('f', leaf(bn, 'd'), vlit(zd(A.val[p], A.im(p))), xval(A.idx[p])));
       }
     }
     // frozen product
@@ -593,6 +652,20 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
     << "// n=" << A.n << " nnz=" << A.nnz() << " K=" << S.K << " B=" << B << " U=" << U << " M=" << S.M
     << " mode=" << S.mode << "\n";
   o << "typedef unsigned long long u64;\n";
+  if (g.cx)  // complex sweep helpers: each op is 2 or 4 DP instructions (counted as such)
+    o << "struct cplx { double re, im; };\n"
+         "__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cplx{a.re + b.re, a.im + b.im}; }\n"
+         "__device__ __forceinline__ cplx csub(cplx a, cplx b) { return cplx{a.re - b.re, a.im - b.im}; }\n"
+         "__device__ __forceinline__ cplx cneg(cplx a) { return cplx{-a.re, -a.im}; }\n"
+         "__device__ __forceinline__ cplx caddr(cplx a, double r) { return cplx{a.re + r, a.im}; }\n"
+         "__device__ __forceinline__ cplx cfmar(double s, double r, cplx x) { return cplx{fma(s, r, x.re), x.im}; }\n"
+         "__device__ __forceinline__ cplx cmul(cplx a, cplx b) {\n"
+         "  return cplx{fma(a.re, b.re, -(a.im * b.im)), fma(a.re, b.im, a.im * b.re)}; }\n"
+         "__device__ __forceinline__ cplx cscale(double s, cplx a) { return cplx{s * a.re, s * a.im}; }\n"
+         "__device__ __forceinline__ cplx cfma_s(double s, cplx a, cplx x) {\n"
+         "  return cplx{fma(s, a.re, x.re), fma(s, a.im, x.im)}; }\n"
+         "__device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx c) {\n"
+         "  return cplx{fma(a.re, b.re, fma(-a.im, b.im, c.re)), fma(a.re, b.im, fma(a.im, b.re, c.im))}; }\n";
   if (g.i01) o << "typedef unsigned __int128 u128;\ntypedef __int128 i128;\n";
   // HYBRID tier: row slot s of this thread at tier[s * (all threads) + thread]
   // (the paper's coalesced x[nthreads * row + tid] layout, Listing 4)
@@ -613,7 +686,7 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
   g.line("t = __shfl_sync(0xffffffffu, t, 0);");
   g.line("if (t >= task_count) break;");
   g.line("const u64 task = task_begin + t;");
-  g.line(std::string(g.PT()) + " lacc = 0;");
+  g.line(std::string(g.PT()) + " lacc = " + g.zero() + ";");
   g.line("#pragma unroll 1");
   g.line("for (unsigned m = 0; m < " + std::to_string(S.M) + "u; ++m) {");
   g.ind = "      ";
@@ -622,12 +695,14 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
   g.ops = 0;
   g.seed();
   kc.ops_seed = g.ops;
-  g.line(std::string(g.PT()) + " cacc = 0;");
+  g.line(std::string(g.PT()) + " cacc = " + g.zero() + ";");
   double ops_body = 0, ops_switch = 0;
   if (U == 0) {
     // B == 0: one product per chunk (h = chunk), everything frozen; sign (-1)^h
     const std::string P = g.has_frozen ? std::string("F") : std::string("1");
-    g.line("cacc = (chunk & 1ull) ? (" + std::string(g.PT()) + ")(0 - " + P + ") : " + P + ";");
+    if (g.cx) g.line("cacc = (chunk & 1ull) ? cneg(" + (g.has_frozen ? P : std::string("cplx{1.0, 0.0}")) +
+                     ") : " + (g.has_frozen ? P : std::string("cplx{1.0, 0.0}")) + ";");
+    else g.line("cacc = (chunk & 1ull) ? (" + std::string(g.PT()) + ")(0 - " + P + ") : " + P + ";");
   } else {
     if (nblk > 1) {
       g.line("#pragma unroll 1");
@@ -665,14 +740,16 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
     else g.line("const double sU = ((h >> " + std::to_string(U) + ") & 1ull) ? -1.0 : 1.0;");
     g.ops = 0;
     g.begin_region();
-    g.block_body();
+    if (g.zs) g.block_zero_skip_body();
+    else g.block_body();
     g.end_region();
     ops_body = g.ops;
     g.ind = "      ";
     g.line("}");
   }
-  if (masked) g.line("if (chunk < " + std::to_string(S.nchunks_total) + "ull) lacc += cacc;");
-  else g.line("lacc += cacc;");
+  const std::string acc_stmt = g.cx ? "lacc = cadd(lacc, cacc);" : "lacc += cacc;";
+  if (masked) g.line("if (chunk < " + std::to_string(S.nchunks_total) + "ull) " + acc_stmt);
+  else g.line(acc_stmt);
   g.ind = "    ";
   g.line("}");
   // fixed-order warp tree (deterministic task slot)
@@ -685,7 +762,14 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
     g.line("}");
   } else {
     g.line("#pragma unroll");
-    g.line("for (int o = 16; o > 0; o >>= 1) lacc += __shfl_xor_sync(0xffffffffu, lacc, o);");
+    if (g.cx) {
+      g.line("for (int o = 16; o > 0; o >>= 1) {");
+      g.line("  lacc.re += __shfl_xor_sync(0xffffffffu, lacc.re, o);");
+      g.line("  lacc.im += __shfl_xor_sync(0xffffffffu, lacc.im, o);");
+      g.line("}");
+    } else {
+      g.line("for (int o = 16; o > 0; o >>= 1) lacc += __shfl_xor_sync(0xffffffffu, lacc, o);");
+    }
   }
   g.line("if (lane == 0) slots[t] = lacc;");
   g.ind = "  ";
@@ -707,14 +791,14 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
   int tier_rows = 0;
   for (int r = 0; r < A.n; ++r) tier_rows += g.tier_slot[r] >= 0;
   kc.tier_rows = tier_rows;
-  kc.tier_bytes = tier_rows * (g.i01 ? 4 : 8);
+  kc.tier_bytes = tier_rows * (g.i01 ? 4 : (g.cx ? 16 : 8));
   kc.live_rows = live - tier_rows;
   kc.levels = (int)g.nonempty.size();
   int qs = 0, ds = 0;
   for (int l : g.nonempty) qs += g.qreg(l) + (l >= 1 && g.sreg(l));
   for (const Factor& f : g.fac) ds += f.group && !f.constant() && f.level >= 0;
-  const int wpv = g.i01 ? 1 : 2;   // 32-bit registers per x value
-  const int wpp = g.i01 ? 4 : 2;   // per product value
+  const int wpv = g.i01 ? 1 : (g.cx ? 4 : 2);   // 32-bit registers per x value
+  const int wpp = g.i01 ? 4 : (g.cx ? 4 : 2);   // per product value
   kc.est_regs = kc.live_rows * wpv + (qs + ds) * wpp + (U + 2) * wpp + 28;
   return kc;
 }

@@ -23,14 +23,41 @@ Csx transpose(const Csx& a) {
   t.val.resize(nnz);
   for (int p = 0; p < nnz; ++p) t.ptr[a.idx[p] + 1]++;
   for (int i = 0; i < n; ++i) t.ptr[i + 1] += t.ptr[i];
+  if (a.complex()) t.vim.resize(nnz);
   std::vector<int32_t> pos(t.ptr.begin(), t.ptr.end() - 1);
   for (int j = 0; j < n; ++j)  // ascending outer index => ascending inner index in t
     for (int p = a.ptr[j]; p < a.ptr[j + 1]; ++p) {
       int q = pos[a.idx[p]]++;
       t.idx[q] = j;
       t.val[q] = a.val[p];
+      if (a.complex()) t.vim[q] = a.vim[p];
     }
   return t;
+}
+
+int validate_and_convert_c(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx, const double* val2,
+                           Csx& ccs, Csx& crs, std::string& err) {
+  if (n < 1 || n > 64 || !ptr) return validate_and_convert(n, fmt, ptr, idx, nullptr, ccs, crs, err);
+  const int nnz = ptr[n] > 0 ? ptr[n] : 0;
+  if (nnz > 0 && !val2) { err = "val is NULL"; return PERM_EINVAL; }
+  std::vector<double> mag(nnz, 1.0);  // structural check with |a| as the value
+  for (int p = 0; p < nnz; ++p) {
+    const double re = val2[2 * p], im = val2[2 * p + 1];
+    if (!std::isfinite(re) || !std::isfinite(im)) { err = "non-finite value"; return PERM_EINVAL; }
+    if (re == 0.0 && im == 0.0) { err = "explicit zero value (formats store nonzeros only)"; return PERM_EINVAL; }
+  }
+  int st = validate_and_convert(n, fmt, ptr, idx, mag.data(), ccs, crs, err);
+  if (st != PERM_OK) return st;
+  Csx in;
+  in.n = n;
+  in.ptr.assign(ptr, ptr + n + 1);
+  in.idx.assign(idx, idx + nnz);
+  in.val.resize(nnz);
+  in.vim.resize(nnz);
+  for (int p = 0; p < nnz; ++p) { in.val[p] = val2[2 * p]; in.vim[p] = val2[2 * p + 1]; }
+  if (fmt == PERM_CCS) { ccs = in; crs = transpose(in); }
+  else { crs = in; ccs = transpose(in); }
+  return PERM_OK;
 }
 
 int validate_and_convert(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
@@ -160,10 +187,14 @@ Csx permute_ccs(const Csx& ccs, const std::vector<int>& rowp, const std::vector<
   o.ptr.assign(1, 0);
   for (int j = 0; j < n; ++j) {
     int oc = colp[j];
-    std::vector<std::pair<int, double>> e;
-    for (int p = ccs.ptr[oc]; p < ccs.ptr[oc + 1]; ++p) e.push_back({rinv[ccs.idx[p]], ccs.val[p]});
+    std::vector<std::pair<int, int>> e;  // (ordered row, source position)
+    for (int p = ccs.ptr[oc]; p < ccs.ptr[oc + 1]; ++p) e.push_back({rinv[ccs.idx[p]], p});
     std::sort(e.begin(), e.end());
-    for (auto& q : e) { o.idx.push_back(q.first); o.val.push_back(q.second); }
+    for (auto& q : e) {
+      o.idx.push_back(q.first);
+      o.val.push_back(ccs.val[q.second]);
+      if (ccs.complex()) o.vim.push_back(ccs.vim[q.second]);
+    }
     o.ptr.push_back((int)o.idx.size());
   }
   return o;

@@ -13,14 +13,22 @@ struct Csx {
   int n = 0;
   std::vector<int32_t> ptr, idx;
   std::vector<double> val;
+  std::vector<double> vim;  // imaginary parts (complex matrices); empty = real
   int nnz() const { return ptr.empty() ? 0 : ptr[n]; }
+  bool complex() const { return !vim.empty(); }
+  double im(int p) const { return vim.empty() ? 0.0 : vim[p]; }
 };
+
+constexpr int PERM_MODE_COMPLEX_INTERNAL = 4;  // complex FP64 sweep (perm_plan_complex)
 
 // ---- matrix.cpp ----------------------------------------------------------
 // Validate a CCS/CRS input (boundary rules of perm.h); on success fill both
 // layouts.  Returns a perm_status; err gets a message.
 int validate_and_convert(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
                          const double* val, Csx& ccs, Csx& crs, std::string& err);
+// complex variant: val2 = interleaved (re, im) pairs, nnz of them
+int validate_and_convert_c(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
+                           const double* val2, Csx& ccs, Csx& crs, std::string& err);
 Csx transpose(const Csx& a);
 int structural_rank(const Csx& ccs);  // Hopcroft-Karp
 void order_permanent(const Csx& ccs, const Csx& crs, std::vector<int>& rowp, std::vector<int>& colp);

@@ -18,9 +18,9 @@
 
 #include "perm_internal.h"
 
-extern "C" cudaError_t libperm_launch_tree_reduce(const void* slots, uint64_t count, int is_u128, void* out,
+extern "C" cudaError_t libperm_launch_tree_reduce(const void* slots, uint64_t count, int kind, void* out,
                                                   cudaStream_t st);
-extern "C" cudaError_t libperm_launch_fold(const void* partials, int world, int n, int is_u128, int neg,
+extern "C" cudaError_t libperm_launch_fold(const void* partials, int world, int n, int kind, int neg,
                                            void* out, cudaStream_t st);
 
 using namespace perm;
@@ -134,7 +134,10 @@ struct perm_plan_s {
   std::vector<char> cubin;
   std::string ptxas_log;
   perm_plan_info info{};
-  bool is_u128 = false;
+  bool is_u128 = false;   // INT01 partials (16 B)
+  bool is_c128 = false;   // complex FP64 partials (re, im; 16 B)
+  int kind() const { return is_u128 ? 1 : (is_c128 ? 2 : 0); }
+  size_t pbytes() const { return (is_u128 || is_c128) ? 16 : 8; }
   // device state
   bool on_device = false;
   int device = 0;
@@ -199,7 +202,7 @@ int load_device(perm_plan_s* p) {
     if (bps < 1) return fail(PERM_ECUDA, "generated kernel cannot be resident (occupancy 0)");
     p->info.blocks_per_sm = bps;
     p->info.grid = bps * p->info.sms;
-    const size_t sb = (p->is_u128 ? 16 : 8) * (size_t)p->info.tasks;
+    const size_t sb = p->pbytes() * (size_t)p->info.tasks;
     CUDA_TRY(cudaMalloc(&p->d_slots, std::max<size_t>(sb, 16)));
     if (p->code.tier_bytes > 0) {
       const size_t tb = (size_t)p->code.tier_bytes * (size_t)p->info.grid * (size_t)p->spec.threads;
@@ -230,7 +233,7 @@ int run_range(perm_plan_s* p, uint64_t first, uint64_t count, double* sweep_ms, 
   CUDA_TRY(cudaEventRecord(p->ev[0], p->stream));
   CUDA_TRY(cudaLaunchKernel((const void*)p->kern, dim3(grid), dim3(p->spec.threads), args, 0, p->stream));
   CUDA_TRY(cudaEventRecord(p->ev[1], p->stream));
-  CUDA_TRY(libperm_launch_tree_reduce(p->d_slots, count, p->is_u128, p->d_partial, p->stream));
+  CUDA_TRY(libperm_launch_tree_reduce(p->d_slots, count, p->kind(), p->d_partial, p->stream));
   CUDA_TRY(cudaEventRecord(p->ev[2], p->stream));
   if (sweep_ms || reduce_ms) {
     CUDA_TRY(cudaEventSynchronize(p->ev[2]));
@@ -273,6 +276,7 @@ void fill_result(perm_plan_s* p, perm_result* r, const unsigned char* raw16, boo
     double v;
     std::memcpy(&v, raw16, 8);
     r->value = v;
+    if (p->is_c128) std::memcpy(&r->value_im, raw16 + 8, 8);
   }
   (void)scaled;
 }
@@ -325,8 +329,10 @@ int perm_alg2_launch_parameters(uint64_t tau, int n, uint64_t* out, int cap) {
   return alg2_launch_parameters(tau, n, out, cap);
 }
 
-int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx, const double* val,
-                 perm_ordering ord, const perm_opts* opts_in, perm_plan_t* out) {
+}  // extern "C"
+
+static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx, const double* val,
+                     bool complex_input, perm_ordering ord, const perm_opts* opts_in, perm_plan_t* out) {
   if (!out) return fail(PERM_EINVAL, "out is NULL");
   *out = nullptr;
   const double t0 = now_ms();
@@ -337,7 +343,8 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     return code;
   };
   std::string err;
-  int st = validate_and_convert(n, fmt, ptr, idx, val, p->ccs, p->crs, err);
+  int st = complex_input ? validate_and_convert_c(n, fmt, ptr, idx, val, p->ccs, p->crs, err)
+                         : validate_and_convert(n, fmt, ptr, idx, val, p->ccs, p->crs, err);
   if (st != PERM_OK) { delete p; return fail(st, err); }
   p->n = n;
   perm_plan_info& I = p->info;
@@ -350,6 +357,13 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
   // ---- mode
   int mode = p->opts.mode;
   if (mode < PERM_MODE_AUTO || mode > PERM_MODE_INT01) { delete p; return fail(PERM_EINVAL, "unknown mode"); }
+  if (complex_input) {
+    if (mode == PERM_MODE_INT01 || mode == PERM_MODE_HYBRID) {
+      delete p;
+      return fail(PERM_EINVAL, "complex matrices support modes AUTO/REG only");
+    }
+    mode = PERM_MODE_COMPLEX_INTERNAL;
+  }
   if (mode == PERM_MODE_AUTO) mode = (all_ones(p->ccs) && int01_fits(p->crs)) ? PERM_MODE_INT01 : PERM_MODE_REG;
   if (mode == PERM_MODE_INT01) {
     if (!all_ones(p->ccs)) { delete p; return fail(PERM_EINVAL, "INT01 mode needs every value == 1.0"); }
@@ -360,6 +374,7 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
   }
   I.mode = mode;
   p->is_u128 = mode == PERM_MODE_INT01;
+  p->is_c128 = mode == PERM_MODE_COMPLEX_INTERNAL;
 
   // ---- geometry for a sweep over nb h-bits: B, U, M, tasks (Lemma 1 aligned
   // chunks; DESIGN "Chunk grid").  Depends only on (n, K, opts): identical on
@@ -377,7 +392,9 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     if (B > nb) B = nb;
     // INT01 keeps 128-bit products: a shorter unrolled block (fewer live
     // 4-register values, faster NVRTC)
-    int U = p->opts.block_log2 > 0 ? p->opts.block_log2 : (mode == PERM_MODE_INT01 ? 3 : 5);
+    int U = p->opts.block_log2 > 0
+                ? p->opts.block_log2
+                : ((mode == PERM_MODE_INT01 || mode == PERM_MODE_COMPLEX_INTERNAL) ? 3 : 5);
     if (U > B) U = B;
     const uint64_t nchunks = 1ull << (nb - B);
     const uint64_t warp_chunks = std::max<uint64_t>(1, nchunks / 32);
@@ -422,14 +439,21 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
   if (ord < PERM_ORDER_NONE || ord > PERM_ORDER_AUTO) { delete p; return fail(PERM_EINVAL, "unknown ordering"); }
   auto make_x0 = [&](const Csx& o) {  // Alg. 1 lines 1-5 (reading R1: true a_{i,n-1})
     Csx orr = transpose(o);
-    std::vector<double> x0(n);
+    const bool cpx = mode == PERM_MODE_COMPLEX_INTERNAL;
+    std::vector<double> x0(cpx ? 2 * n : n);  // complex: (re, im) pairs
     for (int i = 0; i < n; ++i) {
-      long double sum = 0, last = 0;
+      long double sum = 0, last = 0, sumi = 0, lasti = 0;
       for (int q = orr.ptr[i]; q < orr.ptr[i + 1]; ++q) {
         sum += orr.val[q];
-        if (orr.idx[q] == n - 1) last = orr.val[q];
+        sumi += orr.im(q);
+        if (orr.idx[q] == n - 1) { last = orr.val[q]; lasti = orr.im(q); }
       }
-      x0[i] = mode == PERM_MODE_INT01 ? (double)(2 * last - sum) : (double)(last - sum / 2);
+      if (cpx) {
+        x0[2 * i] = (double)(last - sum / 2);
+        x0[2 * i + 1] = (double)(lasti - sumi / 2);
+      } else {
+        x0[i] = mode == PERM_MODE_INT01 ? (double)(2 * last - sum) : (double)(last - sum / 2);
+      }
     }
     return x0;
   };
@@ -446,6 +470,7 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     app(p->ccs.ptr.data(), p->ccs.ptr.size() * sizeof(int32_t));
     app(p->ccs.idx.data(), p->ccs.idx.size() * sizeof(int32_t));
     app(p->ccs.val.data(), p->ccs.val.size() * sizeof(double));
+    app(p->ccs.vim.data(), p->ccs.vim.size() * sizeof(double));
   }
   bool plan_hit = false;
   {
@@ -660,6 +685,8 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
     if (n == 1) p->trivial1 = true;
     I.codegen_ms = now_ms() - tc - I.nvrtc_ms;
     I.w_alg1 = w_alg1(p->occs);
+    if (p->is_c128)  // complex Alg. 1: an update is 2 DP ops, a product step 4, the accumulate 2
+      I.w_alg1 = 2.0 * (I.w_alg1 - n) + 4.0 * (n - 1) + 2.0;
     if (!p->singular && !p->trivial1) {
       I.w_plan = p->code.w_plan;
       I.reg_rows = p->code.live_rows;
@@ -682,12 +709,24 @@ int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx,
   return PERM_OK;
 }
 
+extern "C" {
+
+int perm_plan_ex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx, const double* val,
+                 perm_ordering ord, const perm_opts* opts, perm_plan_t* out) {
+  return plan_impl(n, fmt, ptr, idx, val, false, ord, opts, out);
+}
+
+int perm_plan_complex(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx, const double* val_re_im,
+                      perm_ordering ord, const perm_opts* opts, perm_plan_t* out) {
+  return plan_impl(n, fmt, ptr, idx, val_re_im, true, ord, opts, out);
+}
+
 int perm_plan(int n, perm_format fmt, const int32_t* ptr, const int32_t* idx, const double* val,
               perm_ordering ord, perm_plan_t* out) {
   return perm_plan_ex(n, fmt, ptr, idx, val, ord, nullptr, out);
 }
 
-int perm_partial_bytes(perm_plan_t p) { return p && p->is_u128 ? 16 : 8; }
+int perm_partial_bytes(perm_plan_t p) { return p ? (int)p->pbytes() : 8; }
 
 int perm_shard_range(perm_plan_t p, int rank, int world, uint64_t* first_task, uint64_t* ntasks,
                      uint64_t* g_begin, uint64_t* g_end) {
@@ -710,8 +749,8 @@ int perm_shard_range(perm_plan_t p, int rank, int world, uint64_t* first_task, u
 }
 
 double perm_fold_host(perm_plan_t p, const double* partials, int world) {
-  if (!p || !partials || p->is_u128 || world < 1 || world > 65536 || (world & (world - 1))) {
-    g_err = "perm_fold_host: FP64 plan and power-of-two world <= 65536 required";
+  if (!p || !partials || p->is_u128 || p->is_c128 || world < 1 || world > 65536 || (world & (world - 1))) {
+    g_err = "perm_fold_host: real FP64 plan and power-of-two world <= 65536 required";
     return std::nan("");
   }
   if (p->singular) return 0.0;
@@ -736,7 +775,7 @@ int perm_compute_shard_async(perm_plan_t p, int rank, int world, void* d_partial
   int st = shard_range(p, rank, world, first, count);
   if (st) return st;
   CUDA_TRY(cudaSetDevice(p->device));
-  const size_t pb = p->is_u128 ? 16 : 8;
+  const size_t pb = p->pbytes();
   if (p->trivial1 || p->singular) {
     // unscaled partial: singular -> 0.  n == 1: the fold scales by
     // 4(1 mod 2) - 2 = 2 (FP64) or shifts by n-1 = 0 (INT01), so the partial
@@ -744,7 +783,10 @@ int perm_compute_shard_async(perm_plan_t p, int rank, int world, void* d_partial
     unsigned char raw[16] = {0};
     if (p->trivial1 && rank == 0) {
       if (p->is_u128) { __int128 w = (long long)p->ccs.val[0]; std::memcpy(raw, &w, 16); }
-      else { double v = p->ccs.val[0] / 2.0; std::memcpy(raw, &v, 8); }
+      else {
+        const double v[2] = {p->ccs.val[0] / 2.0, p->ccs.im(0) / 2.0};
+        std::memcpy(raw, v, 16);
+      }
     }
     CUDA_TRY(cudaMemcpyAsync(d_partial, raw, pb, cudaMemcpyHostToDevice, p->stream));
     p->last_count = 0;
@@ -790,7 +832,7 @@ int perm_fold_async(perm_plan_t p, const void* d_partials, int world, void* d_ou
     return fail(PERM_EINVAL, "world must be a power of two <= 65536");
   CUDA_TRY(cudaSetDevice(p->device));
   const int nn = p->trivial1 ? 1 : p->n;
-  CUDA_TRY(libperm_launch_fold(d_partials, world, nn, p->is_u128, p->info.K & 1, d_out, p->stream));
+  CUDA_TRY(libperm_launch_fold(d_partials, world, nn, p->kind(), p->info.K & 1, d_out, p->stream));
   return PERM_OK;
 }
 
@@ -807,13 +849,14 @@ int perm_fold(perm_plan_t p, const perm_result* shards, int world, perm_result* 
     CUDA_TRY(cudaMalloc(&p->d_scratch, p->scratch_bytes));
   }
   std::vector<unsigned char> raw(16 * world, 0);
-  const size_t pb = p->is_u128 ? 16 : 8;
+  const size_t pb = p->pbytes();
   for (int k = 0; k < world; ++k) {
     if (p->is_u128) {
       std::memcpy(&raw[pb * k], &shards[k].exact_lo, 8);
       std::memcpy(&raw[pb * k + 8], &shards[k].exact_hi, 8);
     } else {
       std::memcpy(&raw[pb * k], &shards[k].value, 8);
+      if (p->is_c128) std::memcpy(&raw[pb * k + 8], &shards[k].value_im, 8);
     }
   }
   CUDA_TRY(cudaSetDevice(p->device));
@@ -824,7 +867,7 @@ int perm_fold(perm_plan_t p, const perm_result* shards, int world, perm_result* 
   CUDA_TRY(cudaMemcpyAsync(res, p->d_partial, 16, cudaMemcpyDeviceToHost, p->stream));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   fill_result(p, out, res, true);
-  if (p->singular) { out->value = 0.0; out->exact_lo = out->exact_hi = 0; }
+  if (p->singular) { out->value = 0.0; out->value_im = 0.0; out->exact_lo = out->exact_hi = 0; }
   out->world = world;
   out->products = p->n >= 2 ? (1ull << (p->n - 1)) : 1;
   for (int k = 0; k < world; ++k) {
@@ -852,7 +895,7 @@ int perm_debug_task_partials(perm_plan_t p, void* host, uint64_t cap, uint64_t* 
   if (!p || !count) return fail(PERM_EINVAL, "NULL argument");
   if (!p->on_device) return fail(PERM_ECUDA, "plan has no device state");
   const uint64_t c = std::min(cap, p->last_count);
-  const size_t pb = p->is_u128 ? 16 : 8;
+  const size_t pb = p->pbytes();
   if (c && host) {
     CUDA_TRY(cudaSetDevice(p->device));
     CUDA_TRY(cudaStreamSynchronize(p->stream));

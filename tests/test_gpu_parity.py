@@ -315,3 +315,76 @@ def test_config5_band44_vs_band_dp():
     exp = oracle.perm_band(A, w)
     v = plan(A, mode="reg").compute()
     assert rel(v, exp) < REL
+
+
+# ---- complex permanents (boson sampling) -----------------------
+
+def crel(a, b, scale=None):
+    return abs(a - b) / (scale if scale is not None else max(abs(b), 1e-300))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7])
+def test_complex_tiny_vs_naive(n):
+    A = synth.erdos_renyi_complex(n, 0.7, n)
+    v = plan(A).compute()
+    assert isinstance(v, complex)
+    exp = oracle.perm_naive_complex(A)
+    assert crel(v, exp) < 1e-12
+
+
+@pytest.mark.parametrize("n,p,seed", [(16, 0.3, 1), (22, 0.25, 2), (26, 0.2, 3)])
+def test_complex_er_vs_oracle(n, p, seed):
+    A = synth.erdos_renyi_complex(n, p, seed)
+    exp, sabs = oracle.perm_nw_complex(A)
+    for fc in (-1, 0):
+        P = plan(A, factor_cols=fc)
+        assert P.info["mode"] == 4
+        v = P.compute()
+        assert crel(v, exp) < REL, (fc, v, exp, sabs / abs(exp))
+
+
+def test_complex_closed_forms():
+    z = 0.6 + 0.3j
+    n = 14
+    assert crel(plan(z * np.ones((n, n))).compute(), math.factorial(n) * z ** n) < 1e-12
+    D = np.diag(np.exp(1j * np.arange(1, 21)) * np.linspace(0.5, 1.5, 20))
+    assert crel(plan(D).compute(), complex(np.prod(np.diag(D)))) < 1e-13
+
+
+@pytest.mark.parametrize("n,depth,seed", [(20, 3, 1), (30, 4, 2)])
+def test_complex_unitary_brickwork_vs_band_dp(n, depth, seed):
+    U = synth.unitary_brickwork(n, depth, seed)
+    exp = oracle.perm_band_complex(U, synth.half_bandwidth(U))
+    assert crel(plan(U).compute(), exp) < REL
+
+
+def test_complex_shards_fold_bitwise_and_partials():
+    A = synth.erdos_renyi_complex(30, 0.2, 7)
+    P = plan(A)
+    full = P.compute_ex()
+    for world in (2, 8):
+        f = P.fold([P.shard(r, world) for r in range(world)])
+        assert f.value == full.value and f.value_im == full.value_im
+    P.compute()
+    info = P.info
+    B = oracle_ordered(A, info)
+    first, _ = P.task_partials(cap=0)
+    L = 32 * info["M"] * (1 << info["B"]) << info["K"]
+    # task partials (interleaved re, im) of the whole run
+    import ctypes
+    buf = np.zeros(2 * info["tasks"], np.float64)
+    cnt, fst = ctypes.c_uint64(), ctypes.c_uint64()
+    pb._abi.lib().perm_debug_task_partials(P.handle, buf.ctypes.data, info["tasks"], ctypes.byref(cnt),
+                                           ctypes.byref(fst))
+    sign = -1.0 if info["K"] % 2 else 1.0
+    for t in (0, int(cnt.value) - 1, int(cnt.value) // 3):
+        exp, sabs = oracle.nw_range_complex(B, t * L, (t + 1) * L)
+        got = complex(buf[2 * t], buf[2 * t + 1]) * sign
+        assert abs(got - exp) <= 1e-11 * sabs
+
+
+@pytest.mark.slow
+def test_complex_boson_sampling_band44():
+    U = synth.unitary_brickwork(44, 4, 1)
+    exp = oracle.perm_band_complex(U, synth.half_bandwidth(U))
+    assert crel(plan(U).compute(), exp) < REL

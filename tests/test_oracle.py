@@ -352,3 +352,12 @@ def test_complex_block_diagonal_product():
     exp = brute_perm_c(B1) * brute_perm_c(B2)
     v, sabs = oracle.perm_nw_complex(A)
     assert abs(v - exp) <= 1e-14 * sabs
+
+
+def test_complex_band_dp_vs_naive_and_nw():
+    U = synth.unitary_brickwork(12, 3, 2)
+    w = synth.half_bandwidth(U)
+    b = oracle.perm_band_complex(U, w)
+    v, sabs = oracle.perm_nw_complex(U)
+    assert abs(b - v) <= 1e-14 * sabs
+    assert abs(b - oracle.perm_naive_complex(U)) <= 1e-14 * sabs
