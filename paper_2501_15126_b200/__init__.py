@@ -273,10 +273,12 @@ class Plan:
         _check(L.perm_debug_task_partials(self.handle, None, 0, ctypes.byref(cnt), ctypes.byref(first)),
                "perm_debug_task_partials")
         # query count with cap 0 returns 0; ask again with the real cap
-        buf = np.zeros(cap * (pb // 8), np.uint64 if pb == 16 else np.float64)
+        buf = np.zeros(cap * (pb // 8), np.uint64 if (pb == 16 and not self.is_complex) else np.float64)
         _check(L.perm_debug_task_partials(self.handle, buf.ctypes.data, cap, ctypes.byref(cnt),
                                           ctypes.byref(first)), "perm_debug_task_partials")
         c = cnt.value
+        if self.is_complex:
+            return first.value, buf[:2 * c].view(np.complex128).copy()
         if pb == 16:
             lo = buf[0:2 * c:2].astype(object)
             hi = buf[1:2 * c:2].astype(object)
