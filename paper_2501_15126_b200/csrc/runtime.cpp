@@ -517,7 +517,10 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     // reduced geometry), until no candidate helps.
     // search knobs (env overrides for tuning experiments)
     const int elim_cands = getenv("PERM_ELIM_CANDS") ? atoi(getenv("PERM_ELIM_CANDS")) : 6;
-    const int elim_maxsize = getenv("PERM_ELIM_MAXSIZE") ? atoi(getenv("PERM_ELIM_MAXSIZE")) : 96;
+    // complex values take 4 registers: halve the composite size bound
+    const int elim_maxsize = getenv("PERM_ELIM_MAXSIZE") ? atoi(getenv("PERM_ELIM_MAXSIZE"))
+                                                         : (mode == PERM_MODE_COMPLEX_INTERNAL ? 40 : 96);
+    const int elim_beam = std::max(1, getenv("PERM_ELIM_BEAM") ? atoi(getenv("PERM_ELIM_BEAM")) : 1);
     auto greedy_elim = [&](const std::vector<int>& rp, const std::vector<int>& cp) {
       std::vector<int> seq;
       if (kcap == 0) return seq;
@@ -531,34 +534,42 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         set_hybrid(sp, o);
         return generate_kernel(o, make_x0(o), sp).w_plan;
       };
-      double cur = evalW(seq);
-      while ((int)seq.size() < kcap && (int)seq.size() < n - 3) {
-        const int k = (int)seq.size();
-        std::vector<int> cand;
-        std::vector<int> fc = factored_columns(cp, seq, k);
-        for (int q = k; q < n - 1 && (int)cand.size() < elim_cands; ++q) cand.push_back(fc[q]);
-        std::vector<int> cs = costsort_swept(p->ccs, fc, k);
-        for (int q = k, added = 0; q < n - 1 && added < elim_cands; ++q, ++added)
-          if (std::find(cand.begin(), cand.end(), cs[q]) == cand.end()) cand.push_back(cs[q]);
-        double bw = 1e300;
-        int bc = -1;
-        std::vector<std::pair<int, std::future<double>>> jobs;  // candidates evaluated concurrently
-        for (int c : cand) {
-          std::vector<int> s2 = seq;
-          s2.push_back(c);
-          // bound the composite factors' evaluation size (code size, registers)
-          if (elim_eval_size(p->ccs, factored_columns(cp, s2, k + 1), k + 1) > elim_maxsize) continue;
-          jobs.emplace_back(c, std::async(std::launch::async, evalW, s2));
+      // beam search (width 1 = greedy) over elimination sequences
+      std::vector<std::pair<double, std::vector<int>>> beam = {{evalW(seq), seq}};
+      std::pair<double, std::vector<int>> best = beam[0];
+      while ((int)beam[0].second.size() < kcap && (int)beam[0].second.size() < n - 3) {
+        const int k = (int)beam[0].second.size();
+        std::vector<std::pair<std::vector<int>, std::future<double>>> jobs;  // evaluated concurrently
+        std::set<std::vector<int>> seen;
+        for (const auto& st : beam) {
+          const std::vector<int>& s = st.second;
+          std::vector<int> cand;
+          std::vector<int> fc = factored_columns(cp, s, k);
+          for (int q = k; q < n - 1 && (int)cand.size() < elim_cands; ++q) cand.push_back(fc[q]);
+          std::vector<int> cs = costsort_swept(p->ccs, fc, k);
+          for (int q = k, added = 0; q < n - 1 && added < elim_cands; ++q, ++added)
+            if (std::find(cand.begin(), cand.end(), cs[q]) == cand.end()) cand.push_back(cs[q]);
+          for (int c : cand) {
+            std::vector<int> s2 = s;
+            s2.push_back(c);
+            std::vector<int> key = s2;
+            std::sort(key.begin(), key.end());  // the elimination set decides the tree up to order
+            if (!seen.insert(key).second) continue;
+            // bound the composite factors' evaluation size (code size, registers)
+            if (elim_eval_size(p->ccs, factored_columns(cp, s2, k + 1), k + 1) > elim_maxsize) continue;
+            jobs.emplace_back(s2, std::async(std::launch::async, evalW, s2));
+          }
         }
-        for (auto& j : jobs) {
-          const double w = j.second.get();
-          if (w < bw) { bw = w; bc = j.first; }
-        }
-        if (bc < 0 || !(bw < cur * 0.995)) break;
-        seq.push_back(bc);
-        cur = bw;
+        std::vector<std::pair<double, std::vector<int>>> next;
+        for (auto& j : jobs) next.push_back({j.second.get(), j.first});
+        if (next.empty()) break;
+        std::sort(next.begin(), next.end());
+        if (!(next[0].first < best.first * 0.995)) break;  // no further gain
+        best = next[0];
+        if ((int)next.size() > elim_beam) next.resize(elim_beam);
+        beam.swap(next);
       }
-      return seq;
+      return best.second;
     };
     std::map<int, std::vector<int>> elim_of_base;
     for (int base : bases) {
@@ -647,6 +658,14 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     std::vector<std::future<Built>> fut;  // candidates compiled concurrently (NVRTC is thread-safe)
     for (const Cand& c : cands) fut.push_back(std::async(std::launch::async, build, c));
     for (size_t ci = 0; ci < cands.size(); ++ci) {
+      if (ci + 1 == cands.size() && !have && cands[ci].K > 0 && fut.size() == cands.size()) {
+        // every elimination candidate spilled: fall back to the plain sweep (K = 0)
+        Cand plain = cands[ci];
+        plain.K = 0;
+        plain.var = 0;
+        cands.push_back(plain);
+        fut.push_back(std::async(std::launch::async, build, plain));
+      }
       Built b = fut[ci].get();
       const Cand& c = cands[ci];
       if (b.status != PERM_OK) {
