@@ -222,7 +222,8 @@ def to_ccs(A: np.ndarray):
         idx.extend(rows.tolist())
         val.extend(A[rows, j].tolist())
         ptr.append(len(idx))
-    return (np.array(ptr, dtype=np.int32), np.array(idx, dtype=np.int32), np.array(val, dtype=np.float64))
+    vdt = np.complex128 if np.iscomplexobj(A) else np.float64
+    return (np.array(ptr, dtype=np.int32), np.array(idx, dtype=np.int32), np.array(val, dtype=vdt))
 
 
 def to_crs(A: np.ndarray):

@@ -34,6 +34,14 @@ def main():
     run("0/1 ER n=36 p=0.2 int01 no zero-skip", synth.erdos_renyi(36, 0.2, 1, binary=True), mode="int01",
         zero_skip=-1)
     run("0/1 ER n=40 p=0.2 int01", synth.erdos_renyi(40, 0.2, 1, binary=True), mode="int01")
+    run("0/1 ER n=40 p=0.2 int01 no zero-skip", synth.erdos_renyi(40, 0.2, 1, binary=True), mode="int01",
+        zero_skip=-1)
+    run("0/1 ER n=40 p=0.1 int01", synth.erdos_renyi(40, 0.1, 2, binary=True), mode="int01")
+    run("0/1 ER n=40 p=0.1 int01 no zero-skip", synth.erdos_renyi(40, 0.1, 2, binary=True), mode="int01",
+        zero_skip=-1)
+    run("0/1 band n=44 w=4 int01", (synth.givens_brickwork(44, 4, 1) != 0).astype(float), mode="int01")
+    run("complex unitary brickwork n=44 depth 4", synth.unitary_brickwork(44, 4, 1))
+    run("complex ER n=32 p=0.2", synth.erdos_renyi_complex(32, 0.2, 1))
     run("0/1 ER n=36 p=0.2 fp64", synth.erdos_renyi(36, 0.2, 1, binary=True), mode="reg")
     run("n=44 p=0.2", synth.erdos_renyi(44, 0.2, 1), mode="reg")
 
