@@ -516,12 +516,15 @@ struct Gen {
   void block_body() {
     std::vector<int> stack(U + 1, -1);
     const int npairs = 1 << (U - 1);
+    const bool dbg = getenv("PERM_DEBUG_OPS") != nullptr;
     for (int k = 0; k < npairs; ++k) {
       const int u = 2 * k;
+      const double ops0 = ops;
       if (u > 0) {
         int b = __builtin_ctz(u);
         std::string sg = (b == U - 1) ? "sU" : (((u >> (b + 1)) & 1) ? "-" : "+");
         flip(b, sg);
+        if (dbg) fprintf(stderr, "[ops] pair %d flip bit %d: %.0f\n", k, b, ops - ops0);
       }
       // pair: product at even step u (current state), flip bit 0, product at u+1
       std::string sg0 = (U >= 2) ? ((((u + 1) >> 1) & 1) ? "-" : "+") : "sU";
@@ -555,6 +558,7 @@ struct Gen {
         ++lvl;
       }
       stack[lvl] = v;
+      if (dbg) fprintf(stderr, "[ops] pair %d total %.0f\n", k, ops - ops0);
     }
     set("cacc", add(reg("cacc", pty()), stack[U - 1]));
   }
