@@ -49,6 +49,7 @@
 #include <set>
 #include <sstream>
 #include <complex>
+#include <functional>
 #include <tuple>
 
 #include "perm_internal.h"
@@ -186,6 +187,7 @@ struct Gen {
     for (int l = 0; l < B; ++l)
       if (!G[l].empty()) (l < cT ? nonempty : tier_levels).push_back(l);
     zs = i01 && S.zero_skip && U >= 2;
+    build_cc();
     tier_slot.assign(n, -1);
     int slots = 0;
     for (int l : tier_levels)
@@ -424,7 +426,109 @@ struct Gen {
   void recompute_factor(int f) {
     const Factor& F = fac[f];
     if (!F.group || F.constant() || tierf(f) || zs0(f)) return;
+    if (ccon(f)) { cc_update(f, {}, true); return; }
     set(dv(f), group_value(f));
+  }
+
+  // ---- composite caches (DESIGN 3.12): for a register-resident composite root
+  // E = prod_c c(in) - prod_c c(out), its direct children are grouped by the
+  // lowest in-chunk swept bit touching them; level products (in/out) and
+  // suffix products over child levels are cached, so a flip re-evaluates only
+  // the touched children and the suffix chain below them.
+  struct CCache {
+    std::vector<int> lev;                // distinct child levels, ascending (B = never in-chunk)
+    std::vector<std::vector<int>> ch;    // children per level
+    std::map<int, int> idx_of_child;     // child node -> level index
+  };
+  std::vector<CCache> cc;
+  std::vector<int> cc_child_of_row;      // row -> direct child (of its root) containing it
+  bool ccon(int f) const {
+    if (!S.cc || !fac[f].group || fac[f].constant() || fac[f].level < 0 || tierf(f) || cc[f].lev.size() < 2)
+      return false;
+    const Node& N = nodes[fac[f].node];  // two-leaf roots keep their 2-FMA closed form
+    return !(N.ch.size() == 2 && nodes[N.ch[0]].leaf && nodes[N.ch[1]].leaf);
+  }
+  // rows changed by a flip -> composite-cache updates (touched level indices)
+  void update_factors(const std::map<int, std::vector<int>>& rows_by_fac) {
+    for (auto& kv : rows_by_fac) {
+      const int f = kv.first;
+      if (!ccon(f)) { recompute_factor(f); continue; }
+      std::set<int> touched;
+      for (int r : kv.second) touched.insert(cc[f].idx_of_child.at(cc_child_of_row[r]));
+      cc_update(f, touched, false);
+    }
+  }
+  std::string ccn(const char* t, int f, int i) const {
+    return std::string(t) + std::to_string(fac[f].col) + "_" + std::to_string(i);
+  }
+  bool cc_qreg(int f, int i) const {  // cache the level product unless it is a single leaf
+    return cc[f].ch[i].size() > 1 || !nodes[cc[f].ch[i][0]].leaf;
+  }
+  std::map<int, zd> cc_shift(int f) {  // the root's column switched in
+    std::map<int, zd> s;
+    for (auto& kv : colval[fac[f].col]) s[kv.first] = i01 ? zd(2.0) : kv.second;
+    return s;
+  }
+  int cc_levprod(int f, int i, bool in) {  // product of the children at level index i, fresh
+    std::vector<int> v;
+    const std::map<int, zd> sh = in ? cc_shift(f) : std::map<int, zd>();
+    for (int c : cc[f].ch[i]) v.push_back(node_value(c, sh));
+    return prod(v);
+  }
+  int cc_q(int f, int i, bool in) {
+    if (cc_qreg(f, i)) return reg(ccn(in ? "qI" : "qO", f, i), pty());
+    return cc_levprod(f, i, in);
+  }
+  int cc_s(int f, int i, bool in) {  // suffix product over levels >= i
+    if (i + 1 >= (int)cc[f].lev.size()) return cc_q(f, i, in);
+    return reg(ccn(in ? "sI" : "sO", f, i), pty());
+  }
+  // touched: level indices whose children changed; all = recompute every level
+  void cc_update(int f, const std::set<int>& touched, bool all) {
+    const int m = (int)cc[f].lev.size();
+    int h = -1;
+    for (int i = 0; i < m; ++i) {
+      if (!all && !touched.count(i)) continue;
+      h = std::max(h, i);
+      if (cc_qreg(f, i)) {
+        set(ccn("qI", f, i), cc_levprod(f, i, true));
+        set(ccn("qO", f, i), cc_levprod(f, i, false));
+      }
+    }
+    for (int i = std::min(h, m - 2); i >= 0; --i) {
+      set(ccn("sI", f, i), mul(cc_q(f, i, true), cc_s(f, i + 1, true)));
+      set(ccn("sO", f, i), mul(cc_q(f, i, false), cc_s(f, i + 1, false)));
+    }
+    set(dv(f), sub(cc_s(f, 0, true), cc_s(f, 0, false)));
+  }
+  void build_cc() {
+    cc.assign(fac.size(), {});
+    cc_child_of_row.assign(n, -1);
+    std::vector<int> rowlev(n, B);
+    for (int b = B - 1; b >= 0; --b)
+      for (auto& kv : colval[K + b]) rowlev[kv.first] = b;
+    std::function<void(int, int, int&)> scan = [&](int nd, int top, int& lv) {
+      if (nodes[nd].leaf) {
+        lv = std::min(lv, rowlev[nodes[nd].row]);
+        cc_child_of_row[nodes[nd].row] = top;
+        return;
+      }
+      for (int c : nodes[nd].ch) scan(c, top, lv);
+    };
+    for (int f = 0; f < (int)fac.size(); ++f) {
+      if (!fac[f].group || fac[f].constant()) continue;
+      std::map<int, std::vector<int>> bylev;
+      for (int c : nodes[fac[f].node].ch) {
+        int lv = B;
+        scan(c, c, lv);
+        bylev[lv].push_back(c);
+      }
+      for (auto& kv : bylev) {
+        for (int c : kv.second) cc[f].idx_of_child[c] = (int)cc[f].lev.size();
+        cc[f].lev.push_back(kv.first);
+        cc[f].ch.push_back(kv.second);
+      }
+    }
   }
 
   // one update y_r +-= a_rj.  sign: "+", "-" (static) or a runtime +-1 register
@@ -448,11 +552,13 @@ struct Gen {
   void flip(int b, const std::string& sign) {
     const int j = K + b;
     std::set<int> facs, levels;
+    std::map<int, std::vector<int>> rows_by_fac;
     for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) {
       update(A.idx[p], p, sign);
       facs.insert(fac_of_row[A.idx[p]]);
+      if (!dead_row(A.idx[p])) rows_by_fac[fac_of_row[A.idx[p]]].push_back(A.idx[p]);
     }
-    for (int f : facs) recompute_factor(f);
+    update_factors(rows_by_fac);
     bool tier_touched = false;
     for (int f : facs) {
       if (fac[f].level < 0) continue;  // constant D_k: unchanged
@@ -531,12 +637,12 @@ struct Gen {
       const int e = qval(0);
       {
         const int j = K;
-        std::set<int> facs;
+        std::map<int, std::vector<int>> rows_by_fac;
         for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p) {
           update(A.idx[p], p, sg0);
-          facs.insert(fac_of_row[A.idx[p]]);
+          if (!dead_row(A.idx[p])) rows_by_fac[fac_of_row[A.idx[p]]].push_back(A.idx[p]);
         }
-        for (int f : facs) recompute_factor(f);
+        update_factors(rows_by_fac);
         recompute_q(0);
       }
       const int d = sub(e, qval(0));
@@ -603,8 +709,10 @@ struct Gen {
     }
     // live groups, level products, suffix chain
     for (int f = 0; f < (int)fac.size(); ++f)
-      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f) && !zs0(f))
-        cur[dv(f)] = group_value(f);
+      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f) && !zs0(f)) {
+        if (ccon(f)) cc_update(f, {}, true);
+        else cur[dv(f)] = group_value(f);
+      }
     if (has_tier()) recompute_sg();
     for (int l : nonempty)
       if (qreg(l)) {
@@ -621,8 +729,19 @@ struct Gen {
       else line(std::string(VT()) + " " + xv(r) + " = " + nm(cur[xv(r)]) + ";");
     }
     for (int f = 0; f < (int)fac.size(); ++f)
-      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f) && !zs0(f))
+      if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f) && !zs0(f)) {
         line(std::string(PT()) + " " + dv(f) + " = " + nm(cur[dv(f)]) + ";");
+        if (!ccon(f)) continue;
+        const int m = (int)cc[f].lev.size();
+        for (int i = 0; i < m; ++i) {
+          if (cc_qreg(f, i))
+            for (const char* t : {"qI", "qO"})
+              line(std::string(PT()) + " " + ccn(t, f, i) + " = " + nm(cur[ccn(t, f, i)]) + ";");
+          if (i + 1 < m)
+            for (const char* t : {"sI", "sO"})
+              line(std::string(PT()) + " " + ccn(t, f, i) + " = " + nm(cur[ccn(t, f, i)]) + ";");
+        }
+      }
     if (has_tier()) line(std::string(PT()) + " SG = " + nm(cur["SG"]) + ";");
     for (int l : nonempty)
       if (qreg(l)) line(std::string(PT()) + " Q" + std::to_string(l) + " = " + nm(cur["Q" + std::to_string(l)]) + ";");

@@ -59,7 +59,8 @@ struct KernelSpec {
   int mode = PERM_MODE_REG;    // REG / HYBRID / INT01
   int hybrid_c = 0;            // HYBRID: factors of levels >= hybrid_c live in the global tier
   int threads = 128;           // threads per block
-  bool zero_skip = false;      // INT01: warp-uniform skip of pairs whose product above level 0 is 0
+  bool zero_skip = false;      // INT01: warp-uniform skip of blocks whose product above them is 0
+  bool cc = false;             // composite caches (level/suffix products inside composite roots)
   int min_blocks = 1;          // __launch_bounds__ second argument
   uint64_t nchunks_total = 0;  // 2^(n-1-B)
 };

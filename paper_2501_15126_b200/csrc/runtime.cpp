@@ -503,7 +503,9 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       const int r8 = (std::max(regs, 16) + 7) / 8 * 8;
       return std::max(1, std::min(16, 65536 / (threads * r8)));
     };
-    struct Cand { double score, w; int base, K, var, bcap, est; };
+    struct Cand { double score, w; int base, K, var, bcap, est; bool cc; };
+    // composite caches (DESIGN 3.12): candidates with and without
+    const bool cc_allowed = !(getenv("PERM_NO_CC") && atoi(getenv("PERM_NO_CC")) == 1);
     std::vector<Cand> cands;
     // swept-column variants: 0 = base order, 1 = sorted by flip cost (AUTO only)
     const int nvar = ord == PERM_ORDER_AUTO ? 2 : 1;
@@ -531,6 +533,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         KernelSpec sp;
         geometry(k, sp, 8);
         sp.U = std::min(sp.U, 4);
+        sp.cc = cc_allowed;
         set_hybrid(sp, o);
         return generate_kernel(o, make_x0(o), sp).w_plan;
       };
@@ -588,9 +591,12 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
             geometry(K, sp, bc);
             set_hybrid(sp, o);
             if (!seenB.insert(sp.B).second) continue;  // cap not binding: duplicate
-            KernelCode kc = generate_kernel(o, xo, sp);
-            const double score = kc.w_plan / eff(bps_of(kc.est_regs, sp.threads));
-            cands.push_back({score, kc.w_plan, base, K, var, bc, kc.est_regs});
+            for (int ccv = 0; ccv < (K > 0 && cc_allowed ? 2 : 1); ++ccv) {
+              sp.cc = ccv == 1;
+              KernelCode kc = generate_kernel(o, xo, sp);
+              const double score = kc.w_plan / eff(bps_of(kc.est_regs, sp.threads));
+              cands.push_back({score, kc.w_plan, base, K, var, bc, kc.est_regs, sp.cc});
+            }
           }
         }
     }
@@ -626,6 +632,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       b.o = permute_ccs(p->ccs, b.rp, b.colp);
       b.xo = make_x0(b.o);
       b.tasks = geometry(c.K, b.sp, c.bcap);
+      b.sp.cc = c.cc;
       set_hybrid(b.sp, b.o);
       if (n == 1 || p->singular) { b.ok = true; return b; }
       int stack = 0, spill = 0;
