@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--chunk-log2", type=int, default=0)
     ap.add_argument("--block-log2", type=int, default=0)
     ap.add_argument("--task-chunks", type=int, default=0)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo + --same-device: test the multi-rank path with ranks sharing one GPU")
+    ap.add_argument("--same-device", action="store_true")
     return ap.parse_args()
 
 
@@ -181,10 +184,15 @@ def main():
     import torch.distributed as dist
     import paper_2501_15126_b200 as pb
 
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     A, cfg = workload(args)
     n = A.shape[0]
     steps_per_perm = 2 ** (n - 1) - 1
@@ -269,6 +277,15 @@ def main():
         achieved = info["w_plan"] * products / (sw / 1000.0) / 1e12
         sm_max = clocks.get("sm_max_mhz") or 1965.0
         peak = info["sms"] * 64 * sm_max * 1e6 / 1e12
+        # DRAM traffic per launch from the committed `ncu --set full` capture of
+        # this same kernel (profiles/), when the plan signature matches
+        traffic, traffic_src = None, None
+        tpath = os.path.join(ROOT, "profiles", "r1_bench_kernel_ncu.json")
+        if os.path.exists(tpath):
+            t = json.load(open(tpath))
+            sig = {k: info[k] for k in ("n", "nnz", "K", "B", "U", "M", "tasks")}
+            if t.get("signature") == sig:
+                traffic, traffic_src = t["dram_bytes_per_launch"], t["source"]
         line = {
             "metric": "gray_steps_per_s", "value": value, "unit": "Gray-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
@@ -285,7 +302,7 @@ def main():
                        "vs_baseline_ref": "paper CodeGen-Hybrid A100 n=40 p=0.2: 3.94 s (P:627), context only"},
             "result": result,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "kernel": "perm_sweep (generated)", "sweep_ms_avg": sw,
                          "peak_def": f"{info['sms']} SMs x 64 FP64 lanes x {sm_max:.0f} MHz, 1 op per "
                                      "DADD/DMUL/DFMA lane-op (datasheet FP64 / 2)",

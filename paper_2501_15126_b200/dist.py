@@ -26,8 +26,15 @@ class ShardedPermanent:
         import torch.distributed as dist
         self.plan.shard_async(self.rank, self.world, self.part.data_ptr())
         if self.world > 1:
-            dist.all_gather_into_tensor(self.gathered[: self.world * self.words], self.part[: self.words],
-                                        group=self.group)
+            if dist.get_backend(self.group) == "gloo":   # test path (ranks sharing one GPU): host staging
+                host = self.part[: self.words].cpu()
+                outs = [host.clone() for _ in range(self.world)]
+                dist.all_gather(outs, host, group=self.group)
+                self.gathered[: self.world * self.words].copy_(
+                    __import__("torch").cat(outs).to(self.gathered.device))
+            else:
+                dist.all_gather_into_tensor(self.gathered[: self.world * self.words], self.part[: self.words],
+                                            group=self.group)
             src = self.gathered
         else:
             src = self.part
