@@ -283,7 +283,7 @@ def main():
         tpath = os.path.join(ROOT, "profiles", "r1_bench_kernel_ncu.json")
         if os.path.exists(tpath):
             t = json.load(open(tpath))
-            sig = {k: info[k] for k in ("n", "nnz", "K", "B", "U", "M", "tasks")}
+            sig = {k: info[k] for k in ("n", "nnz", "K", "B", "U", "M", "tasks", "w_plan")}
             if t.get("signature") == sig:
                 traffic, traffic_src = t["dram_bytes_per_launch"], t["source"]
         line = {

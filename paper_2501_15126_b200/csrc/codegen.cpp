@@ -43,7 +43,9 @@
 //  * Lane partials: pairwise inside a block, sequential over blocks and chunks,
 //    then a fixed xor-shuffle tree per warp-task (deterministic slot).
 #include <algorithm>
+#include <cctype>
 #include <cmath>
+#include <cstring>
 #include <cstdio>
 #include <map>
 #include <set>
@@ -51,6 +53,7 @@
 #include <complex>
 #include <functional>
 #include <tuple>
+#include <unordered_map>
 
 #include "perm_internal.h"
 
@@ -117,6 +120,7 @@ struct Gen {
   std::map<std::string, int> cur;        // register -> current value id
   std::set<std::string> dirty;
   int tmp = 0;
+  std::map<std::string, double> wt;      // temporary -> executed DP instructions
 
   std::vector<Node> nodes;
   typedef std::complex<double> zd;
@@ -296,6 +300,7 @@ struct Gen {
     }
     ops += w;
     std::string name = "t" + std::to_string(tmp++);
+    wt[name] = w;
     line(std::string("const ") + tyname(ty) + " " + name + " = " + expr + ";");
     vals.push_back({op, a, b, c, ty, name});
     return memo[key] = (int)vals.size() - 1;
@@ -323,6 +328,13 @@ struct Gen {
     cur.clear();
     dirty.clear();
   }
+  // region marker for the post-pass: ops of region k execute `weight` times per chunk
+  std::vector<double> region_weight;
+  void mark_region(double weight) {
+    o << "//@R" << region_weight.size() << "\n";
+    region_weight.push_back(weight);
+  }
+
   void end_region() {  // write loop-carried registers (and tier rows) back
     for (const std::string& r : dirty) {
       const int id = cur[r];
@@ -673,6 +685,7 @@ struct Gen {
   void seed() {
     const int nbits = n - 1 - K;
     line("const u64 gr = h0 ^ (h0 >> 1);");
+    mark_region(1.0);
     begin_region();
     for (int r = 0; r < n; ++r) {
       if (dead_row(r)) continue;
@@ -751,6 +764,223 @@ struct Gen {
     dirty.clear();
   }
 };
+
+// ---- whole-kernel post-pass ----------------------------------------------------
+// 1. Dead-code elimination.  Composite caches and level registers can end up
+//    written but never read (e.g. a composite whose value only enters through
+//    its cached in/out suffixes); nvcc would drop them, so W_plan would count
+//    instructions that never execute.  Registers with no read and temporaries
+//    with no use are removed to a fixpoint.
+// 2. FMA contraction (real FP64 only).  With --fmad=false nothing is
+//    contracted behind our back, so the generator contracts itself: a product
+//    tA = X * Y used exactly once, by tC = tA +- tB (or tB +- tA) in the same
+//    straight-line segment (no brace between them), becomes
+//    tC = fma(X, Y, +-tB) (or fma(-X, Y, tB)): one DP instruction and one
+//    rounding fewer.
+// 3. The surviving temporaries' instruction weights give the executed DP
+//    instructions per region (W_plan stays equal to ncu's executed count) and
+//    the surviving loop-carried registers give the register estimate.
+struct PostStats {
+  std::vector<double> region_ops;
+  int reg_words = 0;   // 32-bit words of surviving loop-carried registers
+  int fused = 0, removed = 0;
+};
+
+PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, size_t nregions, bool fuse) {
+  PostStats ps;
+  ps.region_ops.assign(nregions, 0.0);
+  struct Ln {
+    std::string text;
+    int region = -1, kind = 0;  // 1 const def, 2 register decl, 3 register assign
+    int name = -1;              // defined / assigned identifier
+    std::vector<int> toks;      // identifier ids on the line (all occurrences)
+    bool alive = true;
+  };
+  std::unordered_map<std::string, int> ids;
+  std::vector<std::string> idname;
+  auto intern = [&](const std::string& s) {
+    auto it = ids.find(s);
+    if (it != ids.end()) return it->second;
+    ids.emplace(s, (int)idname.size());
+    idname.push_back(s);
+    return (int)idname.size() - 1;
+  };
+  auto isid0 = [](char c) { return std::isalpha((unsigned char)c) || c == '_'; };
+  auto isid = [](char c) { return std::isalnum((unsigned char)c) || c == '_'; };
+  std::vector<Ln> L;
+  {
+    std::istringstream is(src);
+    std::string s;
+    int region = -1;
+    while (std::getline(is, s)) {
+      if (s.compare(0, 3, "//@") == 0) {
+        region = std::atoi(s.c_str() + 4);
+        continue;
+      }
+      Ln l;
+      l.text = s;
+      l.region = region;
+      for (size_t i = 0; i < s.size();) {
+        if (isid0(s[i]) && (i == 0 || !isid(s[i - 1]))) {
+          size_t j = i;
+          while (j < s.size() && isid(s[j])) ++j;
+          l.toks.push_back(intern(s.substr(i, j - i)));
+          i = j;
+        } else if (std::isdigit((unsigned char)s[i])) {
+          while (i < s.size() && (isid(s[i]) || s[i] == '.')) ++i;
+        } else {
+          ++i;
+        }
+      }
+      L.push_back(std::move(l));
+    }
+  }
+  std::vector<int> occ(idname.size(), 0), ndef(idname.size(), 0);
+  std::vector<char> is_reg(idname.size(), 0);
+  const int id_const = ids.count("const") ? ids["const"] : -2;
+  auto tyword = [&](int id) {
+    const std::string& w = idname[id];
+    return w == "double" || w == "u128" || w == "cplx" || w == "int";
+  };
+  for (Ln& l : L) {
+    for (int t : l.toks) ++occ[t];
+    if (l.region < 0 || l.toks.empty() || l.text.empty() || l.text.back() != ';') continue;
+    const size_t eq = l.text.find(" = ");
+    if (eq == std::string::npos) continue;
+    if (l.toks.size() >= 3 && l.toks[0] == id_const && tyword(l.toks[1])) {
+      l.kind = 1;
+      l.name = l.toks[2];
+    } else if (l.toks.size() >= 2 && tyword(l.toks[0]) && l.region == 0) {
+      const std::string& nmv = idname[l.toks[1]];
+      if (nmv != "cacc" && nmv != "lacc") {
+        l.kind = 2;
+        l.name = l.toks[1];
+        is_reg[l.name] = 1;
+      }
+    }
+  }
+  for (Ln& l : L)
+    if (l.kind == 0 && l.region >= 0 && !l.toks.empty() && is_reg[l.toks[0]] && l.text.back() == ';' &&
+        l.text.find(" = ") != std::string::npos &&
+        l.text.find_first_not_of(' ') == l.text.find(idname[l.toks[0]])) {
+      l.kind = 3;
+      l.name = l.toks[0];
+    }
+  for (const Ln& l : L)
+    if (l.kind == 2 || l.kind == 3) ++ndef[l.name];
+  auto kill = [&](Ln& l) {
+    l.alive = false;
+    for (int t : l.toks) --occ[t];
+    if (l.kind == 2 || l.kind == 3) --ndef[l.name];
+    ++ps.removed;
+  };
+  if (!getenv("PERM_NO_DCE")) {
+    for (bool changed = true; changed;) {
+      changed = false;
+      for (Ln& l : L)  // registers never read
+        if (l.alive && (l.kind == 2 || l.kind == 3) && occ[l.name] == ndef[l.name]) {
+          kill(l);
+          changed = true;
+        }
+      for (size_t k = L.size(); k-- > 0;) {  // unused temporaries (uses follow definitions)
+        Ln& l = L[k];
+        if (l.alive && l.kind == 1 && occ[l.name] == 1) {
+          kill(l);
+          changed = true;
+        }
+      }
+    }
+  }
+  if (fuse) {
+    std::unordered_map<int, int> def_line;
+    std::vector<int> seg(L.size(), 0);
+    int sg = 0;
+    for (size_t k = 0; k < L.size(); ++k) {
+      if (!L[k].alive) continue;
+      if (L[k].text.find_first_of("{}") != std::string::npos) ++sg;
+      seg[k] = sg;
+      if (L[k].kind == 1) def_line[L[k].name] = (int)k;
+    }
+    const std::string pre = "const double ";
+    struct Bin { std::string a, op, b, indent; };
+    auto parse = [&](const Ln& l, Bin& b) {
+      const size_t p = l.text.find(pre);
+      if (p == std::string::npos || l.text.find_first_not_of(' ') != p) return false;
+      const size_t eq = l.text.find(" = ", p);
+      const std::string e = l.text.substr(eq + 3, l.text.size() - eq - 4);
+      std::istringstream es(e);
+      std::vector<std::string> tok;
+      std::string t;
+      while (es >> t) tok.push_back(t);
+      if (tok.size() != 3 || tok[1].size() != 1 || !std::strchr("*+-", tok[1][0])) return false;
+      b = {tok[0], tok[1], tok[2], l.text.substr(0, p)};
+      return true;
+    };
+    auto single_mul = [&](const std::string& v, int sgu, Bin& m) -> int {
+      auto it = ids.find(v);
+      if (it == ids.end() || occ[it->second] != 2) return -1;
+      auto d = def_line.find(it->second);
+      if (d == def_line.end() || !L[d->second].alive || seg[d->second] != sgu) return -1;
+      if (!parse(L[d->second], m) || m.op != "*") return -1;
+      return d->second;
+    };
+    for (size_t k = 0; k < L.size(); ++k) {
+      Ln& l = L[k];
+      Bin c, m;
+      if (!l.alive || l.kind != 1 || !parse(l, c) || c.op == "*") continue;
+      const std::string name = idname[l.name];
+      const std::string neg = c.op == "-" ? "-" : "";
+      int d = single_mul(c.a, seg[k], m);
+      std::string text;
+      if (d >= 0) {
+        text = c.indent + pre + name + " = fma(" + m.a + ", " + m.b + ", " + neg + c.b + ");";
+      } else if ((d = single_mul(c.b, seg[k], m)) >= 0) {
+        text = c.indent + pre + name + " = fma(" + neg + m.a + ", " + m.b + ", " + c.a + ");";
+      } else {
+        continue;
+      }
+      // the consumer now reads X, Y instead of tA; the product line goes
+      const int ta = L[d].name;
+      kill(L[d]);
+      --ps.removed;
+      for (size_t q = 0; q < l.toks.size(); ++q)
+        if (l.toks[q] == ta) {
+          l.toks.erase(l.toks.begin() + q);
+          --occ[ta];
+          break;
+        }
+      for (const std::string* v : {&m.a, &m.b})
+        if (!v->empty() && isid0((*v)[0])) {
+          const int id = intern(*v);
+          if (id >= (int)occ.size()) occ.resize(id + 1, 0);
+          l.toks.push_back(id);
+          ++occ[id];
+        }
+      ++ps.fused;
+      l.text = text;
+    }
+  }
+  std::string out;
+  out.reserve(src.size());
+  for (const Ln& l : L) {
+    if (!l.alive) continue;
+    out += l.text;
+    out += '\n';
+    if (l.kind == 1 && l.region >= 0 && l.region < (int)nregions) {
+      auto it = wt.find(idname[l.name]);
+      if (it != wt.end()) ps.region_ops[l.region] += it->second;
+    }
+    if (l.kind == 2) {
+      const std::string& ty = idname[l.toks[0]];
+      ps.reg_words += ty == "int" ? 1 : (ty == "double" ? 2 : 4);
+    }
+  }
+  src.swap(out);
+  if (getenv("PERM_DEBUG_POST"))
+    fprintf(stderr, "[post] lines %zu regions %zu removed %d fused %d regwords %d\n", L.size(), nregions,
+            ps.removed, ps.fused, ps.reg_words);
+  return ps;
+}
 
 }  // namespace
 
@@ -843,6 +1073,7 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
         std::string save = g.ind;
         g.ind += "  ";
         g.ops = 0;
+        g.mark_region((double)(1ull << (B - 1 - b)));
         g.begin_region();
         g.flip(b, "s");
         g.end_region();
@@ -862,6 +1093,7 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
     if (g.i01) g.line("const int sU = ((h >> " + std::to_string(U) + ") & 1ull) ? -2 : 2;");
     else g.line("const double sU = ((h >> " + std::to_string(U) + ") & 1ull) ? -1.0 : 1.0;");
     g.ops = 0;
+    g.mark_region((double)nblk);
     g.begin_region();
     if (g.zs) g.block_zero_skip_body();
     else g.block_body();
@@ -900,8 +1132,14 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
   o << "}\n";
 
   kc.source = o.str();
-  kc.ops_block = ops_body;
-  const double chunk_ops = kc.ops_seed + (double)nblk * ops_body + ops_switch + 1.0;  // + lacc
+  (void)ops_body;
+  (void)ops_switch;
+  const bool fuse = !g.i01 && !g.cx && !getenv("PERM_NO_FUSE");
+  const PostStats ps = post_pass(kc.source, g.wt, g.region_weight.size(), fuse);
+  double chunk_ops = 1.0;  // + lacc
+  for (size_t k = 0; k < ps.region_ops.size(); ++k) chunk_ops += ps.region_ops[k] * g.region_weight[k];
+  kc.ops_seed = ps.region_ops.empty() ? 0.0 : ps.region_ops[0];
+  kc.ops_block = (U > 0 && ps.region_ops.size() > 1) ? ps.region_ops.back() : 0.0;
   kc.ops_chunk_total = chunk_ops;
   kc.w_plan = chunk_ops / std::ldexp(1.0, B + S.K);  // per Gray step of the full range
   int live = 0, frozen_rows = 0;
@@ -922,7 +1160,12 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
   for (const Factor& f : g.fac) ds += f.group && !f.constant() && f.level >= 0;
   const int wpv = g.i01 ? 1 : (g.cx ? 4 : 2);   // 32-bit registers per x value
   const int wpp = g.i01 ? 4 : (g.cx ? 4 : 2);   // per product value
-  kc.est_regs = kc.live_rows * wpv + (qs + ds) * wpp + (U + 2) * wpp + 28;
+  (void)wpv;
+  (void)qs;
+  (void)ds;
+  // surviving loop-carried registers (rows, level / suffix products, composite
+  // values and caches) + the pairwise-accumulation stack + addressing
+  kc.est_regs = ps.reg_words + (U + 2) * wpp + 28;
   return kc;
 }
 

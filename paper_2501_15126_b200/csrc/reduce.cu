@@ -13,44 +13,38 @@
 
 namespace {
 
-constexpr int RT = 1024;  // reduction threads (one block)
+constexpr int RT = 1024;  // INT01 reduction threads (one block)
 
-// pairwise sum of in[b, b+len) (len a power of two) with a binary-counter
-// stack; element i of the partial array is in[i * stride + comp]
-__device__ double seg_pairwise(const double* __restrict__ in, int stride, int comp, uint64_t b, uint64_t len,
-                               uint64_t count) {
-  double st[40];
-  for (uint64_t k = 0; k < len; ++k) {
-    uint64_t i = b + k;
-    double v = i < count ? in[i * stride + comp] : 0.0;
-    int lvl = 0;
-    uint64_t kk = k;
-    while (kk & 1) { v = st[lvl] + v; kk >>= 1; ++lvl; }
-    st[lvl] = v;
-  }
-  int top = 0;
-  while ((1ull << top) < len) ++top;
-  return st[top];
-}
+// One level-group of the fixed pairwise tree: block b reduces the aligned
+// segment [b*2*RB, (b+1)*2*RB) of the (zero-padded) partial array to one value
+// (thread t adds the adjacent pair (2t, 2t+1) from one coalesced 16-byte
+// load, then a shared-memory tree with adjacent pairing).  Aligned
+// power-of-two segments are complete subtrees of the whole tree, so chaining
+// passes until one value is left gives exactly the tree over all `count`
+// partials (zero padding is exact: v + 0 = v).  Element i of the partial array
+// is in[i * stride + comp]; blockIdx.y = comp.
+constexpr int RB = 256;
 
-// one block; component `comp` of `stride`-double partials; blockIdx.x = comp
-__global__ void __launch_bounds__(RT) tree_reduce_f64(const double* __restrict__ in, int stride, uint64_t count,
-                                                      uint64_t pow2, double* __restrict__ out) {
-  __shared__ double s[RT];
-  const int t = threadIdx.x, comp = blockIdx.x;
-  double v;
-  if (pow2 <= RT) {
-    v = (uint64_t)t < count ? in[(uint64_t)t * stride + comp] : 0.0;
+__global__ void __launch_bounds__(RB) tree_pass_f64(const double* __restrict__ in, int stride, uint64_t count,
+                                                    double* __restrict__ out) {
+  __shared__ double s[RB];
+  const int t = threadIdx.x, comp = blockIdx.y;
+  const uint64_t i = ((uint64_t)blockIdx.x * RB + t) * 2;
+  double a = 0.0, b = 0.0;
+  if (stride == 1 && i + 1 < count) {
+    const double2 v = *reinterpret_cast<const double2*>(in + i);
+    a = v.x;
+    b = v.y;
   } else {
-    const uint64_t seg = pow2 / RT;
-    v = seg_pairwise(in, stride, comp, (uint64_t)t * seg, seg, count);
+    if (i < count) a = in[i * stride + comp];
+    if (i + 1 < count) b = in[(i + 1) * stride + comp];
   }
-  s[t] = v;
-  for (int h = 1; h < RT; h <<= 1) {
+  s[t] = a + b;
+  for (int h = 1; h < RB; h <<= 1) {
     __syncthreads();
     if ((t & (2 * h - 1)) == 0) s[t] = s[t] + s[t + h];
   }
-  if (t == 0) out[comp] = s[0];
+  if (t == 0) out[(uint64_t)blockIdx.x * stride + comp] = s[0];
 }
 
 typedef unsigned __int128 u128;
@@ -101,15 +95,34 @@ __global__ void fold_u128(const u128* __restrict__ part, int world, int n, int n
 
 extern "C" {
 
+// bytes of device scratch libperm_launch_tree_reduce needs for `count` partials
+size_t libperm_tree_scratch_bytes(uint64_t count, int kind) {
+  const uint64_t per = 2 * RB;
+  const uint64_t a = (count + per - 1) / per, b = (a + per - 1) / per;
+  return (size_t)(a + b + 2) * (kind == 2 ? 16 : 8);
+}
+
 // kind: 0 = FP64 (8 B), 1 = INT01 u128 (16 B), 2 = complex FP64 (re, im; 16 B)
-cudaError_t libperm_launch_tree_reduce(const void* slots, uint64_t count, int kind, void* out, cudaStream_t st) {
+cudaError_t libperm_launch_tree_reduce(const void* slots, uint64_t count, int kind, void* out, void* scratch,
+                                       cudaStream_t st) {
   if (kind == 1) {
     tree_reduce_u128<<<1, RT, 0, st>>>((const u128*)slots, count, (u128*)out);
-  } else {
-    uint64_t p2 = 1;
-    while (p2 < count) p2 <<= 1;
-    const int stride = kind == 2 ? 2 : 1;
-    tree_reduce_f64<<<stride, RT, 0, st>>>((const double*)slots, stride, count, p2, (double*)out);
+    return cudaGetLastError();
+  }
+  const int stride = kind == 2 ? 2 : 1;
+  const uint64_t per = 2 * RB;
+  if (count == 0) count = 1;  // callers never pass 0; keep the launch well-formed
+  const double* in = (const double*)slots;
+  double* buf[2] = {(double*)scratch, (double*)scratch + ((count + per - 1) / per) * stride};
+  int which = 0;
+  for (;;) {
+    const uint64_t blocks = (count + per - 1) / per;
+    double* dst = blocks == 1 ? (double*)out : buf[which];
+    tree_pass_f64<<<dim3((unsigned)blocks, stride), RB, 0, st>>>(in, stride, count, dst);
+    if (blocks == 1) break;
+    in = dst;
+    count = blocks;
+    which ^= 1;
   }
   return cudaGetLastError();
 }

@@ -19,7 +19,8 @@
 #include "perm_internal.h"
 
 extern "C" cudaError_t libperm_launch_tree_reduce(const void* slots, uint64_t count, int kind, void* out,
-                                                  cudaStream_t st);
+                                                  void* scratch, cudaStream_t st);
+extern "C" size_t libperm_tree_scratch_bytes(uint64_t count, int kind);
 extern "C" cudaError_t libperm_launch_fold(const void* partials, int world, int n, int kind, int neg,
                                            void* out, cudaStream_t st);
 
@@ -149,6 +150,7 @@ struct perm_plan_s {
   unsigned* d_counter = nullptr;
   void* d_partial = nullptr;  // 16 bytes
   void* d_scratch = nullptr;  // fold scratch (world entries)
+  void* d_rscratch = nullptr; // tree-reduction pass buffers
   size_t scratch_bytes = 0;
   void* d_tier = nullptr;     // HYBRID global tier (tier_rows x resident threads)
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -204,6 +206,7 @@ int load_device(perm_plan_s* p) {
     p->info.grid = bps * p->info.sms;
     const size_t sb = p->pbytes() * (size_t)p->info.tasks;
     CUDA_TRY(cudaMalloc(&p->d_slots, std::max<size_t>(sb, 16)));
+    CUDA_TRY(cudaMalloc(&p->d_rscratch, libperm_tree_scratch_bytes(p->info.tasks, p->kind())));
     if (p->code.tier_bytes > 0) {
       const size_t tb = (size_t)p->code.tier_bytes * (size_t)p->info.grid * (size_t)p->spec.threads;
       CUDA_TRY(cudaMalloc(&p->d_tier, tb));
@@ -233,7 +236,7 @@ int run_range(perm_plan_s* p, uint64_t first, uint64_t count, double* sweep_ms, 
   CUDA_TRY(cudaEventRecord(p->ev[0], p->stream));
   CUDA_TRY(cudaLaunchKernel((const void*)p->kern, dim3(grid), dim3(p->spec.threads), args, 0, p->stream));
   CUDA_TRY(cudaEventRecord(p->ev[1], p->stream));
-  CUDA_TRY(libperm_launch_tree_reduce(p->d_slots, count, p->kind(), p->d_partial, p->stream));
+  CUDA_TRY(libperm_launch_tree_reduce(p->d_slots, count, p->kind(), p->d_partial, p->d_rscratch, p->stream));
   CUDA_TRY(cudaEventRecord(p->ev[2], p->stream));
   if (sweep_ms || reduce_ms) {
     CUDA_TRY(cudaEventSynchronize(p->ev[2]));
@@ -969,6 +972,7 @@ void perm_free(perm_plan_t p) {
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->d_slots) cudaFree(p->d_slots);
     if (p->d_counter) cudaFree(p->d_counter);
+    if (p->d_rscratch) cudaFree(p->d_rscratch);
     if (p->d_partial) cudaFree(p->d_partial);
     if (p->d_scratch) cudaFree(p->d_scratch);
     if (p->d_tier) cudaFree(p->d_tier);

@@ -116,7 +116,7 @@ def main():
         A = synth.erdos_renyi(a.dim, a.p, a.seed)
         P = pb.Plan.from_dense(A, mode=a.mode, no_device=True)
         info = P.info
-        sig = {key: info[key] for key in ("n", "nnz", "K", "B", "U", "M", "tasks")}
+        sig = {key: info[key] for key in ("n", "nnz", "K", "B", "U", "M", "tasks", "w_plan")}
         P.close()
         out = {"signature": sig, "dram_bytes_per_launch": traffic,
                "source": f"profiles/{a.round}_ncu_summary.md (ncu --set full, {os.path.basename(a.full)})",
