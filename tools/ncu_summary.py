@@ -92,6 +92,7 @@ def main():
     ap.add_argument("--round", default="r1")
     ap.add_argument("--launches")
     ap.add_argument("--full")
+    ap.add_argument("--dpaudit", help="ncu csv of the dadd/dmul/dfma thread-instruction counters of one sweep")
     ap.add_argument("--dim", type=int, default=40)
     ap.add_argument("--p", type=float, default=0.2)
     ap.add_argument("--seed", type=int, default=1)
@@ -122,6 +123,16 @@ def main():
                "source": f"profiles/{a.round}_ncu_summary.md (ncu --set full, {os.path.basename(a.full)})",
                "fp64_pipe_pct": num(k["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]),
                "kernel_ms": num(k["gpu__time_duration.sum"])}
+        if a.dpaudit:
+            dp = 0.0
+            for r in csv.reader(open(a.dpaudit)):
+                if len(r) > 3 and "perm_sweep" in " ".join(r) and "_pred_on.sum" in " ".join(r):
+                    dp += float(r[-1].replace(",", ""))
+            gray = info["tasks"] * 32 * info["M"] * (1 << info["B"]) * (1 << info["K"])
+            out["dp_thread_inst_per_launch"] = dp
+            out["w_exec"] = dp / gray
+            out["w_exec_over_w_plan"] = out["w_exec"] / info["w_plan"]
+            shutil.copy(a.dpaudit, os.path.join(prof, f"{a.round}_dpaudit_bench.csv"))
         json.dump(out, open(os.path.join(prof, f"{a.round}_bench_kernel_ncu.json"), "w"), indent=1)
         print("\n", json.dumps(out))
 
