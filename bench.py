@@ -161,7 +161,7 @@ def run_reference(args, rank, world):
     cores = oracle.max_threads()
     emit({"impl": "reference", "metric": "gray_steps_per_s", "value": value, "unit": "Gray-steps/s",
           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-          "ms_per_step": 1000.0 * total / value, "higher_is_better": True, "scaling": "weak",
+          "ms_per_step": 1000.0 * total / value, "higher_is_better": True, "scaling": "strong",
           "vs_baseline": None, "dtype": "f80", "data": "synthetic",
           "config": {**cfg, "note": "CPU oracle (test infrastructure) timed as it stands; ms_per_step "
                                     "extrapolates the sampled rate to one full permanent"},

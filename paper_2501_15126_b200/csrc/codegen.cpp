@@ -113,6 +113,7 @@ struct Gen {
     std::string name;
     bool real_lit = false;  // complex literal with zero imaginary part
     double re = 0;          // its real part
+    double lb = 1e9;        // INT01: log2 of a bound on |value| (1e9: unbounded / wrapping u128)
   };
   std::vector<Val> vals;
   std::map<std::tuple<char, int, int, int>, int> memo;
@@ -192,6 +193,14 @@ struct Gen {
       if (!G[l].empty()) (l < cT ? nonempty : tier_levels).push_back(l);
     zs = i01 && S.zero_skip && U >= 2;
     build_cc();
+    if (i01) {
+      std::vector<int> rn(n, 0);
+      for (int q = 0; q < A.nnz(); ++q) ++rn[A.idx[q]];
+      row_lb.assign(n, 0.0);
+      for (int r = 0; r < n; ++r) row_lb[r] = std::log2((double)std::max(rn[r], 1));
+      init_reg_bounds();
+      if (S.reg_lb_extra) for (auto& kv : *S.reg_lb_extra) reg_lb[kv.first] = std::max(reg_lb[kv.first], kv.second);
+    }
     tier_slot.assign(n, -1);
     int slots = 0;
     for (int l : tier_levels)
@@ -207,7 +216,7 @@ struct Gen {
   const char* PT() const { return i01 ? "u128" : (cx ? "cplx" : "double"); }
   const char* VT() const { return i01 ? "int" : (cx ? "cplx" : "double"); }
   const char* tyname(char t) const {
-    return t == 'i' ? "int" : (t == 'u' ? "u128" : (t == 'z' ? "cplx" : "double"));
+    return t == 'i' ? "int" : (t == 'l' ? "i64" : (t == 'u' ? "u128" : (t == 'z' ? "cplx" : "double")));
   }
   char pty() const { return i01 ? 'u' : (cx ? 'z' : 'd'); }
   char xty() const { return i01 ? 'i' : (cx ? 'z' : 'd'); }
@@ -233,17 +242,127 @@ struct Gen {
     return id;
   }
   int vlit(zd v) { return cx ? zlit(v) : lit(v.real()); }  // value literal of the sweep's type
-  int ilit(long long v) { return leaf(std::to_string(v), 'i'); }
-  int ulit(long long v) { return leaf("((u128)" + std::to_string(v) + ")", 'u'); }
+  int ilit(long long v) {
+    const int id = leaf(std::to_string(v), 'i');
+    vals[id].lb = v == 0 ? -100.0 : std::log2(std::fabs((double)v));
+    return id;
+  }
   const std::string& nm(int id) const { return vals[id].name; }
+
+  // ---- INT01 bound-typed integers ------------------------------------------------
+  // Doubled row values are tiny (|x'_r| <= r_r, the row's nonzero count), so
+  // most products fit 32 or 64 bits.  Every value carries log2 of a bound on
+  // its magnitude; an op runs in the narrowest of int / long long / wrapping
+  // u128 that holds its bound (never narrower than its operands).  Exact
+  // while no int/long long overflows; u128 is the ring Z/2^128 the result is
+  // recovered from.  Loop-carried product registers get their type from the
+  // largest bound ever assigned to them (reg_lb, fixed point over
+  // generations: generate_kernel reruns when an assignment exceeds it).
+  std::map<std::string, double> reg_lb;   // input: register -> assumed bound
+  std::map<std::string, double> reg_seen; // output: register -> largest assigned bound
+  std::vector<double> row_lb;             // row -> log2(max(nnz in row, 1))
+  static char ity(double lb) { return lb <= 30.9 ? 'i' : (lb <= 62.9 ? 'l' : 'u'); }
+  static int irank(char t) { return t == 'i' ? 0 : (t == 'l' ? 1 : 2); }
+  static double lsum(double a, double b) {  // log2(2^a + 2^b)
+    const double m = std::max(a, b);
+    return m >= 1e8 ? 1e9 : m + std::log2(1.0 + std::exp2(std::min(a, b) - m));
+  }
+  std::string icast(int v, char rt) const {
+    const char t = vals[v].ty;
+    if (t == rt) return nm(v);
+    if (rt == 'l') return "(i64)" + nm(v);
+    return "(u128)(i128)" + nm(v);
+  }
+  double reg_bound(const std::string& r) const {
+    auto it = reg_lb.find(r);
+    return it == reg_lb.end() ? 1e9 : it->second;
+  }
+  char reg_ty(const std::string& r) const { return r == "cacc" ? 'u' : ity(reg_bound(r)); }
+  std::string rty(const std::string& r) const { return i01 ? tyname(reg_ty(r)) : std::string(PT()); }
+
   int reg(const std::string& r, char ty) {
     auto it = cur.find(r);
     if (it != cur.end()) return it->second;
-    return cur[r] = leaf(r, ty);
+    if (i01 && ty == 'u') {  // product register: typed by its bound
+      const int id = leaf(r, reg_ty(r));
+      vals[id].lb = r == "cacc" ? 1e9 : reg_bound(r);
+      return cur[r] = id;
+    }
+    const int id = leaf(r, ty);
+    if (i01 && ty == 'i' && r.size() > 1 && r[0] == 'x') vals[id].lb = row_lb[std::atoi(r.c_str() + 1)];
+    return cur[r] = id;
   }
   void set(const std::string& r, int id) {
     cur[r] = id;
     dirty.insert(r);
+    if (i01 && r[0] != 'x' && r != "cacc") {  // product registers: record the assigned bound
+      auto it = reg_seen.find(r);
+      if (it == reg_seen.end()) reg_seen[r] = vals[id].lb;
+      else it->second = std::max(it->second, vals[id].lb);
+    }
+  }
+  // semantic bounds of the loop-carried product registers (mirror the
+  // expressions node_value / recompute_* emit; set() records any excess and
+  // generate_kernel then regenerates with the larger bound)
+  double node_lb(int id, const std::map<int, zd>& sh) const {
+    const Node& N = nodes[id];
+    if (N.leaf) return row_lb[N.row];
+    if (N.ch.size() == 1 && nodes[N.ch[0]].leaf) return 1.0;  // the constant 2
+    auto shift = [&](int r) { auto it = sh.find(r); return it == sh.end() ? 0.0 : it->second.real(); };
+    if (N.ch.size() == 2 && nodes[N.ch[0]].leaf && nodes[N.ch[1]].leaf) {
+      const int r1 = nodes[N.ch[0]].row, r2 = nodes[N.ch[1]].row;
+      const double c = std::fabs(std::llround(2 * shift(r1) + 2 * shift(r2) + 4));
+      return lsum(1.0 + lsum(row_lb[r1], row_lb[r2]), c == 0 ? -100.0 : std::log2(c));
+    }
+    std::map<int, zd> shin = sh;
+    for (auto& kv : colval[N.col]) shin[kv.first] += zd(2.0);
+    double in = 0, out = 0;
+    for (int c : N.ch) {
+      in += node_lb(c, shin);
+      out += node_lb(c, sh);
+    }
+    return lsum(in, out);
+  }
+  void init_reg_bounds() {
+    auto fb = [&](int f) {
+      const Factor& F = fac[f];
+      if (!F.group) return row_lb[F.rows[0]];
+      if (F.constant()) return 1.0;
+      return node_lb(F.node, {});
+    };
+    for (int f = 0; f < (int)fac.size(); ++f) {
+      if (!fac[f].group || fac[f].constant()) continue;
+      reg_lb[dv(f)] = fb(f);
+      const int m = (int)cc[f].lev.size();
+      std::vector<double> qi(m, 0), qo(m, 0);
+      const std::map<int, zd> shin = cc_shift(f);
+      for (int i = 0; i < m; ++i)
+        for (int c : cc[f].ch[i]) {
+          qi[i] += node_lb(c, shin);
+          qo[i] += node_lb(c, {});
+        }
+      double si = 0, so = 0;
+      for (int i = m - 1; i >= 0; --i) {
+        si += qi[i];
+        so += qo[i];
+        reg_lb[ccn("qI", f, i)] = qi[i];
+        reg_lb[ccn("qO", f, i)] = qo[i];
+        reg_lb[ccn("sI", f, i)] = si;
+        reg_lb[ccn("sO", f, i)] = so;
+      }
+    }
+    double frozen = 0;
+    for (int f = 0; f < (int)fac.size(); ++f)
+      if (fac[f].level < 0) frozen += fb(f);
+    reg_lb["F"] = frozen;
+    double above_lb = has_frozen ? frozen : 0.0;
+    for (auto it = nonempty.rbegin(); it != nonempty.rend(); ++it) {
+      double q = 0;
+      for (int f : G[*it]) q += fb(f);
+      reg_lb["Q" + std::to_string(*it)] = q;
+      above_lb += q;
+      reg_lb["S" + std::to_string(*it)] = above_lb;
+    }
   }
   int mk(char op, int a, int b, int c = -1) {
     if ((op == '+' || op == '*') && a > b) std::swap(a, b);
@@ -288,14 +407,34 @@ struct Gen {
           }
           break;
       }
+    } else if (i01) {
+      const double la = vals[a].lb, lbv = b >= 0 ? vals[b].lb : -100.0;
+      double lr = op == '*' ? la + lbv : (op == 'h' ? la + 1.0 : lsum(la, lbv));
+      char rt = ity(lr);
+      if (irank(vals[a].ty) > irank(rt)) rt = vals[a].ty;
+      if (b >= 0 && irank(vals[b].ty) > irank(rt)) rt = vals[b].ty;
+      if (rt == 'u') lr = std::min(lr, 1e9);
+      ty = rt;
+      switch (op) {
+        case '+': expr = icast(a, rt) + " + " + icast(b, rt); break;
+        case '-': expr = icast(a, rt) + " - " + icast(b, rt); break;
+        case '*': expr = icast(a, rt) + " * " + icast(b, rt); break;
+        case 'h': expr = "2 * " + icast(a, rt); break;
+      }
+      ops += w;
+      std::string name = "t" + std::to_string(tmp++);
+      wt[name] = w;
+      line(std::string("const ") + tyname(ty) + " " + name + " = " + expr + ";");
+      Val v{op, a, b, c, ty, name};
+      v.lb = lr;
+      vals.push_back(v);
+      return memo[key] = (int)vals.size() - 1;
     } else {
       switch (op) {
         case '+': expr = nm(a) + " + " + nm(b); break;
         case '-': expr = nm(a) + " - " + nm(b); break;
         case '*': expr = nm(a) + " * " + nm(b); break;
         case 'f': expr = "fma(" + nm(a) + ", " + nm(b) + ", " + nm(c) + ")"; break;
-        case 'c': expr = "(u128)(i128)" + nm(a); ty = 'u'; w = 0; break;
-        case 'h': expr = "2 * " + nm(a); break;  // int doubling (INT01)
       }
     }
     ops += w;
@@ -359,7 +498,7 @@ struct Gen {
     vals.push_back({'M', -1, -1, -1, xty(), name});
     return cur[xv(r)] = (int)vals.size() - 1;
   }
-  int pval(int r) { return i01 ? mk('c', xval(r), -1) : xval(r); }  // row value as product type
+  int pval(int r) { return xval(r); }  // row value (INT01: widened by the ops that use it)
   // value of elimination-tree node `id` with row shifts `sh` (ancestors'
   // eliminated columns switched in; INT01 shifts in doubled units)
   int node_value(int id, const std::map<int, zd>& sh) {
@@ -367,18 +506,23 @@ struct Gen {
     auto shift = [&](int r) { auto it = sh.find(r); return it == sh.end() ? zd(0.0) : it->second; };
     if (N.leaf) {
       const zd s = shift(N.row);
-      if (i01) return s == zd(0.0) ? pval(N.row) : mk('c', add(xval(N.row), ilit(std::llround(s.real()))), -1);
+      if (i01) {
+        if (s == zd(0.0)) return pval(N.row);
+        const int v = add(xval(N.row), ilit(std::llround(s.real())));
+        vals[v].lb = std::min(vals[v].lb, row_lb[N.row]);  // another state of row N.row: |.| <= r
+        return v;
+      }
       return s == zd(0.0) ? xval(N.row) : add(xval(N.row), vlit(s));
     }
     const std::map<int, zd>& cv = colval[N.col];
     if (N.ch.size() == 1 && nodes[N.ch[0]].leaf)  // (y + s + a) - (y + s) = a exactly
-      return i01 ? ulit(2) : vlit(cv.at(nodes[N.ch[0]].row));
+      return i01 ? ilit(2) : vlit(cv.at(nodes[N.ch[0]].row));
     if (N.ch.size() == 2 && nodes[N.ch[0]].leaf && nodes[N.ch[1]].leaf) {
       const int r1 = nodes[N.ch[0]].row, r2 = nodes[N.ch[1]].row;
       const zd s1 = shift(r1), s2 = shift(r2);
       if (i01) {  // (x1+s1+2)(x2+s2+2) - (x1+s1)(x2+s2) = 2 (x1 + x2) + (2 s1 + 2 s2 + 4)
         int t = mk('h', add(xval(r1), xval(r2)), -1);
-        return mk('c', add(t, ilit(std::llround(2 * s1.real() + 2 * s2.real() + 4))), -1);
+        return add(t, ilit(std::llround(2 * s1.real() + 2 * s2.real() + 4)));
       }
       // a1 (y2 + s2) + a2 (y1 + s1) + a1 a2: two FMAs, no cancellation
       const zd a1 = cv.at(r1), a2 = cv.at(r2);
@@ -700,6 +844,7 @@ struct Gen {
       std::string bn = "b" + std::to_string(b);
       if (i01) {
         line("const int " + bn + " = (int)((gr >> " + std::to_string(b) + ") & 1ull) << 1;");
+        vals[leaf(bn, 'i')].lb = 1.0;
         for (int p = A.ptr[j]; p < A.ptr[j + 1]; ++p)
           if (!dead_row(A.idx[p])) set(xv(A.idx[p]), add(xval(A.idx[p]), leaf(bn, 'i')));
       } else {
@@ -717,8 +862,9 @@ struct Gen {
       for (int f = 0; f < (int)fac.size(); ++f)
         if (fac[f].level < 0) v.push_back(fac[f].group && !fac[f].constant() ? group_value(f) : fval(f));
       F = prod(v);
-      line(std::string("const ") + PT() + " F = " + nm(F) + ";");
-      cur["F"] = leaf("F", pty());
+      line(std::string("const ") + rty("F") + " F = " + nm(F) + ";");
+      cur.erase("F");
+      reg("F", pty());
     }
     // live groups, level products, suffix chain
     for (int f = 0; f < (int)fac.size(); ++f)
@@ -743,23 +889,23 @@ struct Gen {
     }
     for (int f = 0; f < (int)fac.size(); ++f)
       if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f) && !zs0(f)) {
-        line(std::string(PT()) + " " + dv(f) + " = " + nm(cur[dv(f)]) + ";");
+        line(rty(dv(f)) + " " + dv(f) + " = " + nm(cur[dv(f)]) + ";");
         if (!ccon(f)) continue;
         const int m = (int)cc[f].lev.size();
         for (int i = 0; i < m; ++i) {
           if (cc_qreg(f, i))
             for (const char* t : {"qI", "qO"})
-              line(std::string(PT()) + " " + ccn(t, f, i) + " = " + nm(cur[ccn(t, f, i)]) + ";");
+              line(rty(ccn(t, f, i)) + " " + ccn(t, f, i) + " = " + nm(cur[ccn(t, f, i)]) + ";");
           if (i + 1 < m)
             for (const char* t : {"sI", "sO"})
-              line(std::string(PT()) + " " + ccn(t, f, i) + " = " + nm(cur[ccn(t, f, i)]) + ";");
+              line(rty(ccn(t, f, i)) + " " + ccn(t, f, i) + " = " + nm(cur[ccn(t, f, i)]) + ";");
         }
       }
     if (has_tier()) line(std::string(PT()) + " SG = " + nm(cur["SG"]) + ";");
     for (int l : nonempty)
-      if (qreg(l)) line(std::string(PT()) + " Q" + std::to_string(l) + " = " + nm(cur["Q" + std::to_string(l)]) + ";");
+      if (qreg(l)) line(rty("Q" + std::to_string(l)) + " Q" + std::to_string(l) + " = " + nm(cur["Q" + std::to_string(l)]) + ";");
     for (int l : nonempty)
-      if (l >= 1 && sreg(l)) line(std::string(PT()) + " S" + std::to_string(l) + " = " + nm(cur["S" + std::to_string(l)]) + ";");
+      if (l >= 1 && sreg(l)) line(rty("S" + std::to_string(l)) + " S" + std::to_string(l) + " = " + nm(cur["S" + std::to_string(l)]) + ";");
     (void)F;
     dirty.clear();
   }
@@ -840,7 +986,7 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
   const int id_const = ids.count("const") ? ids["const"] : -2;
   auto tyword = [&](int id) {
     const std::string& w = idname[id];
-    return w == "double" || w == "u128" || w == "cplx" || w == "int";
+    return w == "double" || w == "u128" || w == "cplx" || w == "int" || w == "i64";
   };
   for (Ln& l : L) {
     for (int t : l.toks) ++occ[t];
@@ -972,7 +1118,7 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
     }
     if (l.kind == 2) {
       const std::string& ty = idname[l.toks[0]];
-      ps.reg_words += ty == "int" ? 1 : (ty == "double" ? 2 : 4);
+      ps.reg_words += ty == "int" ? 1 : ((ty == "double" || ty == "i64") ? 2 : 4);
     }
   }
   src.swap(out);
@@ -993,7 +1139,25 @@ double w_alg1(const Csx& A) {
   return w + (n - 1) + 1;
 }
 
-KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const KernelSpec& S) {
+KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, const KernelSpec& S,
+                                std::map<std::string, double>& excess);
+
+KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const KernelSpec& S0) {
+  // INT01: regenerate while an assignment exceeds a register's semantic bound
+  // (never expected; the bounds mirror the emitted expressions)
+  std::map<std::string, double> extra;
+  KernelSpec S = S0;
+  for (int iter = 0;; ++iter) {
+    std::map<std::string, double> excess;
+    S.reg_lb_extra = &extra;
+    KernelCode kc = generate_kernel_once(A, x0, S, excess);
+    if (excess.empty() || iter >= 6) return kc;
+    for (auto& kv : excess) extra[kv.first] = std::max(extra[kv.first], kv.second);
+  }
+}
+
+KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, const KernelSpec& S,
+                                std::map<std::string, double>& excess) {
   Gen g(A, x0, S);
   KernelCode kc;
   const int B = S.B, U = S.U;
@@ -1019,7 +1183,7 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
          "  return cplx{fma(s, a.re, x.re), fma(s, a.im, x.im)}; }\n"
          "__device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx c) {\n"
          "  return cplx{fma(a.re, b.re, fma(-a.im, b.im, c.re)), fma(a.re, b.im, fma(a.im, b.re, c.im))}; }\n";
-  if (g.i01) o << "typedef unsigned __int128 u128;\ntypedef __int128 i128;\n";
+  if (g.i01) o << "typedef unsigned __int128 u128;\ntypedef __int128 i128;\ntypedef long long i64;\n";
   // HYBRID tier: row slot s of this thread at tier[s * (all threads) + thread]
   // (the paper's coalesced x[nthreads * row + tid] layout, Listing 4)
   o << "#define TIER(s) tier[(size_t)(s) * nt_ + gt_]\n";
@@ -1057,16 +1221,21 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
                      ") : " + (g.has_frozen ? P : std::string("cplx{1.0, 0.0}")) + ";");
     else g.line("cacc = (chunk & 1ull) ? (" + std::string(g.PT()) + ")(0 - " + P + ") : " + P + ";");
   } else {
+    // the signs need only bits U..B of h = (chunk << B) | (blk << U): bits
+    // U..B-1 are blk, bit B is chunk bit 0 (= lane bit 0); a 32-bit hu keeps
+    // the 64-bit h0 out of the loop (registers)
+    const std::string hu_init = "const unsigned cb = ((unsigned)lane & 1u) << " + std::to_string(B - U) + ";";
     if (nblk > 1) {
+      g.line(hu_init);
       g.line("#pragma unroll 1");
       g.line("for (unsigned blk = 0; blk < " + std::to_string(nblk) + "u; ++blk) {");
       g.ind = "        ";
-      g.line("const u64 h = h0 | ((u64)blk << " + std::to_string(U) + ");");
+      g.line("const unsigned hu = cb | blk;");
       g.line("if (blk != 0) {");
       g.ind = "          ";
       g.line("const int j = " + std::to_string(U - 1) + " + __ffs(blk);");
-      if (g.i01) g.line("const int s = ((h >> (j + 1)) & 1ull) ? -2 : 2;");
-      else g.line("const double s = ((h >> (j + 1)) & 1ull) ? -1.0 : 1.0;");
+      if (g.i01) g.line("const int s = ((hu >> (j + " + std::to_string(1 - U) + ")) & 1u) ? -2 : 2;");
+      else g.line("const double s = ((hu >> (j + " + std::to_string(1 - U) + ")) & 1u) ? -1.0 : 1.0;");
       g.line("switch (j) {");
       for (int b = U; b < B; ++b) {
         g.line("case " + std::to_string(b) + ": {");
@@ -1086,12 +1255,13 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
       g.ind = "        ";
       g.line("}");
     } else {
+      g.line(hu_init);
       g.line("{");
       g.ind = "        ";
-      g.line("const u64 h = h0;");
+      g.line("const unsigned hu = cb;");
     }
-    if (g.i01) g.line("const int sU = ((h >> " + std::to_string(U) + ") & 1ull) ? -2 : 2;");
-    else g.line("const double sU = ((h >> " + std::to_string(U) + ") & 1ull) ? -1.0 : 1.0;");
+    if (g.i01) g.line("const int sU = (hu & 1u) ? -2 : 2;");
+    else g.line("const double sU = (hu & 1u) ? -1.0 : 1.0;");
     g.ops = 0;
     g.mark_region((double)nblk);
     g.begin_region();
@@ -1131,6 +1301,9 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
   g.line("}");
   o << "}\n";
 
+  if (g.i01)
+    for (auto& kv : g.reg_seen)
+      if (kv.second > g.reg_bound(kv.first) + 1e-9) excess[kv.first] = kv.second;
   kc.source = o.str();
   (void)ops_body;
   (void)ops_switch;

@@ -1,6 +1,7 @@
 // perm_internal.h -- internal types of libperm (not part of the C ABI).
 #pragma once
 #include <cstdint>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -63,6 +64,8 @@ struct KernelSpec {
   bool cc = false;             // composite caches (level/suffix products inside composite roots)
   int min_blocks = 1;          // __launch_bounds__ second argument
   uint64_t nchunks_total = 0;  // 2^(n-1-B)
+  // INT01 (internal to generate_kernel): raised register bounds for a regeneration
+  const std::map<std::string, double>* reg_lb_extra = nullptr;
 };
 
 struct KernelCode {

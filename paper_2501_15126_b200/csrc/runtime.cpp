@@ -147,10 +147,14 @@ struct perm_plan_s {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
   void* d_slots = nullptr;
-  unsigned* d_counter = nullptr;
+  void* d_counter = nullptr;
   void* d_partial = nullptr;  // 16 bytes
   void* d_scratch = nullptr;  // fold scratch (world entries)
   void* d_rscratch = nullptr; // tree-reduction pass buffers
+  // pooled allocation sizes (perm_free returns the buffers to the pool)
+  size_t partial_bytes = 64, counter_bytes = 256, slots_bytes = 0, rscratch_bytes = 0, tier_alloc_bytes = 0;
+  std::string lib_key;        // cubin bytes: key of the shared loaded library
+  bool lib_held = false;
   size_t scratch_bytes = 0;
   void* d_tier = nullptr;     // HYBRID global tier (tier_rows x resident threads)
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -167,7 +171,76 @@ std::map<std::string, perm_plan_s> g_plan_cache;  // guarded by g_cache_mu
     if (e_ != cudaSuccess) return fail(PERM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// ---- process-wide device resources shared by plans -------------------------
+// Loaded sweep libraries are cached by (device, cubin) so re-planning the same
+// matrix (planner cache hit) does not reload the module; device buffers are
+// recycled through a small per-device pool (perm_free synchronises the plan's
+// stream before returning them).  Both are bounded.
+struct LibEntry {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  int regs = 0, local = 0, bps = 0, refs = 0;
+  uint64_t stamp = 0;
+};
+std::mutex g_dev_mu;
+std::map<std::pair<int, std::string>, LibEntry> g_libs;
+uint64_t g_lib_clock = 0;
+std::multimap<std::pair<int, size_t>, void*> g_pool;
+size_t g_pool_bytes = 0;
+constexpr size_t kPoolCap = 256ull << 20;
+constexpr int kIdleLibs = 16;
+
+cudaError_t pool_alloc(int dev, void** ptr, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_pool.find({dev, bytes});
+    if (it != g_pool.end()) {
+      *ptr = it->second;
+      g_pool.erase(it);
+      g_pool_bytes -= bytes;
+      return cudaSuccess;
+    }
+  }
+  return cudaMalloc(ptr, bytes);
+}
+
+void pool_free(int dev, void* ptr, size_t bytes) {
+  if (!ptr) return;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (g_pool_bytes + bytes > kPoolCap) {
+    cudaFree(ptr);
+    return;
+  }
+  g_pool.insert({{dev, bytes}, ptr});
+  g_pool_bytes += bytes;
+}
+
+void lib_release(int dev, const std::string& key) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_libs.find({dev, key});
+  if (it == g_libs.end()) return;
+  it->second.refs -= 1;
+  it->second.stamp = ++g_lib_clock;
+  int idle = 0;
+  for (auto& kv : g_libs) idle += kv.second.refs == 0;
+  while (idle > kIdleLibs) {  // unload the least recently used idle library
+    auto old = g_libs.end();
+    for (auto q = g_libs.begin(); q != g_libs.end(); ++q)
+      if (q->second.refs == 0 && (old == g_libs.end() || q->second.stamp < old->second.stamp)) old = q;
+    cudaLibraryUnload(old->second.lib);
+    g_libs.erase(old);
+    --idle;
+  }
+}
+
+int load_device_impl(perm_plan_s* p);
 int load_device(perm_plan_s* p) {
+  const double t0 = now_ms();
+  const int st = load_device_impl(p);
+  if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] load_device %.3f ms\n", now_ms() - t0);
+  return st;
+}
+int load_device_impl(perm_plan_s* p) {
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0)
@@ -175,12 +248,24 @@ int load_device(perm_plan_s* p) {
   if (p->opts.device < 0 || p->opts.device >= ndev) return fail(PERM_ECUDA, "device ordinal out of range");
   p->device = p->opts.device;
   CUDA_TRY(cudaSetDevice(p->device));
-  cudaDeviceProp prop;
-  CUDA_TRY(cudaGetDeviceProperties(&prop, p->device));
-  if (prop.major != 10 || prop.minor != 0)
+  // single attributes (cudaGetDeviceProperties costs milliseconds per call)
+  int major = 0, minor = 0, sms = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, p->device));
+  CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, p->device));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+  if (major != 10 || minor != 0)
     return fail(PERM_ECUDA, "libperm kernels are built for sm_100a (B200); device is sm_" +
-                                std::to_string(prop.major) + std::to_string(prop.minor));
-  p->info.sms = prop.multiProcessorCount;
+                                std::to_string(major) + std::to_string(minor));
+  p->info.sms = sms;
+  const bool dbg_t = getenv("PERM_DEBUG_TIMING") != nullptr;
+  double tq = now_ms();
+  auto lap = [&](const char* what) {
+    if (!dbg_t) return;
+    cudaDeviceSynchronize();
+    fprintf(stderr, "[timing]   %s %.3f ms\n", what, now_ms() - tq);
+    tq = now_ms();
+  };
+  lap("attributes");
   if (p->opts.cuda_stream) {
     p->stream = (cudaStream_t)p->opts.cuda_stream;
   } else {
@@ -188,30 +273,59 @@ int load_device(perm_plan_s* p) {
     p->own_stream = true;
   }
   for (auto& ev : p->ev) CUDA_TRY(cudaEventCreate(&ev));
-  CUDA_TRY(cudaMalloc(&p->d_partial, 64));
+  lap("stream+events");
+  CUDA_TRY(pool_alloc(p->device, &p->d_partial, p->partial_bytes));
   p->scratch_bytes = 16 * 128;
-  CUDA_TRY(cudaMalloc(&p->d_scratch, p->scratch_bytes));
-  CUDA_TRY(cudaMalloc(&p->d_counter, sizeof(unsigned)));
+  CUDA_TRY(pool_alloc(p->device, &p->d_scratch, p->scratch_bytes));
+  CUDA_TRY(pool_alloc(p->device, &p->d_counter, p->counter_bytes));
   if (!p->singular && !p->trivial1) {
-    CUDA_TRY(cudaLibraryLoadData(&p->lib, p->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-    CUDA_TRY(cudaLibraryGetKernel(&p->kern, p->lib, p->code.name.c_str()));
-    cudaFuncAttributes fa;
-    CUDA_TRY(cudaFuncGetAttributes(&fa, (const void*)p->kern));
-    p->info.regs_per_thread = fa.numRegs;
-    p->info.local_bytes = (int)fa.localSizeBytes;
-    int bps = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void*)p->kern, p->spec.threads, 0));
-    if (bps < 1) return fail(PERM_ECUDA, "generated kernel cannot be resident (occupancy 0)");
-    p->info.blocks_per_sm = bps;
-    p->info.grid = bps * p->info.sms;
-    const size_t sb = p->pbytes() * (size_t)p->info.tasks;
-    CUDA_TRY(cudaMalloc(&p->d_slots, std::max<size_t>(sb, 16)));
-    CUDA_TRY(cudaMalloc(&p->d_rscratch, libperm_tree_scratch_bytes(p->info.tasks, p->kind())));
+    p->lib_key.assign(p->cubin.begin(), p->cubin.end());
+    LibEntry le;
+    bool hit = false;
+    {
+      std::lock_guard<std::mutex> lk(g_dev_mu);
+      auto it = g_libs.find({p->device, p->lib_key});
+      if (it != g_libs.end()) {
+        it->second.refs += 1;
+        le = it->second;
+        hit = true;
+      }
+    }
+    if (!hit) {
+      CUDA_TRY(cudaLibraryLoadData(&le.lib, p->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+      CUDA_TRY(cudaLibraryGetKernel(&le.kern, le.lib, p->code.name.c_str()));
+      cudaFuncAttributes fa;
+      CUDA_TRY(cudaFuncGetAttributes(&fa, (const void*)le.kern));
+      le.regs = fa.numRegs;
+      le.local = (int)fa.localSizeBytes;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&le.bps, (const void*)le.kern, p->spec.threads, 0));
+      le.refs = 1;
+      std::lock_guard<std::mutex> lk(g_dev_mu);
+      auto ins = g_libs.insert({{p->device, p->lib_key}, le});
+      if (!ins.second) {  // another thread loaded it meanwhile: use that one
+        cudaLibraryUnload(le.lib);
+        ins.first->second.refs += 1;
+        le = ins.first->second;
+      }
+    }
+    lap(hit ? "library (cached)" : "library load");
+    p->lib_held = true;
+    p->kern = le.kern;
+    p->info.regs_per_thread = le.regs;
+    p->info.local_bytes = le.local;
+    if (le.bps < 1) return fail(PERM_ECUDA, "generated kernel cannot be resident (occupancy 0)");
+    p->info.blocks_per_sm = le.bps;
+    p->info.grid = le.bps * p->info.sms;
+    p->slots_bytes = std::max<size_t>(p->pbytes() * (size_t)p->info.tasks, 16);
+    CUDA_TRY(pool_alloc(p->device, &p->d_slots, p->slots_bytes));
+    p->rscratch_bytes = libperm_tree_scratch_bytes(p->info.tasks, p->kind());
+    CUDA_TRY(pool_alloc(p->device, &p->d_rscratch, p->rscratch_bytes));
     if (p->code.tier_bytes > 0) {
-      const size_t tb = (size_t)p->code.tier_bytes * (size_t)p->info.grid * (size_t)p->spec.threads;
-      CUDA_TRY(cudaMalloc(&p->d_tier, tb));
+      p->tier_alloc_bytes = (size_t)p->code.tier_bytes * (size_t)p->info.grid * (size_t)p->spec.threads;
+      CUDA_TRY(pool_alloc(p->device, &p->d_tier, p->tier_alloc_bytes));
       p->info.smem_bytes = 0;
     }
+    lap("buffers");
   }
   p->on_device = true;
   return PERM_OK;
@@ -356,6 +470,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
   I.struct_rank = structural_rank(p->ccs);
   I.singular = p->singular = I.struct_rank < n;
   const double gr = p->opts.gr_ratio > 0 ? p->opts.gr_ratio : 16.0;
+  if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] validate+rank %.3f ms\n", now_ms() - t0);
 
   // ---- mode
   int mode = p->opts.mode;
@@ -476,6 +591,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     app(p->ccs.vim.data(), p->ccs.vim.size() * sizeof(double));
   }
   bool plan_hit = false;
+  if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] key %.3f ms\n", now_ms() - t0);
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_plan_cache.find(pkey);
@@ -597,13 +713,20 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
             for (int ccv = 0; ccv < (K > 0 && cc_allowed ? 2 : 1); ++ccv) {
               sp.cc = ccv == 1;
               KernelCode kc = generate_kernel(o, xo, sp);
-              const double score = kc.w_plan / eff(bps_of(kc.est_regs, sp.threads));
+              // estimates above the 255-register cap are optimistic-capped: ptxas
+              // usually fits them (2 blocks of 128); the spill gate escalates if not
+              const double score = kc.w_plan / eff(bps_of(std::min(kc.est_regs, 255), sp.threads));
               cands.push_back({score, kc.w_plan, base, K, var, bc, kc.est_regs, sp.cc});
             }
           }
         }
     }
     std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.score < b.score; });
+    const bool dbg_plan = getenv("PERM_DEBUG_PLAN") != nullptr;
+    if (dbg_plan)
+      for (const Cand& c : cands)
+        fprintf(stderr, "[plan] cand score %.5f w %.5f base %d K %d var %d bcap %d est %d cc %d\n", c.score, c.w,
+                c.base, c.K, c.var, c.bcap, c.est, (int)c.cc);
     if (cands.size() > 3) cands.resize(3);
     if (p->singular || n == 1) cands.resize(std::min<size_t>(cands.size(), 1));
     // compile the top candidates (NVRTC, spill gate with escalation) and keep
@@ -652,7 +775,10 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         if (b.status != PERM_OK) { b.err = g_err; return b; }
         b.nvrtc_ms += ms;
         parse_ptxas(b.log, b.regs, stack, spill);
-        if (stack <= 0 && spill <= 0) { b.ok = true; break; }
+        if (getenv("PERM_DEBUG_PLAN"))
+          fprintf(stderr, "[plan]   attempt K %d B %d U %d minb %d cc %d: regs %d stack %d spill %d\n", c.K, b.sp.B,
+                  b.sp.U, b.sp.min_blocks, (int)b.sp.cc, b.regs, stack, spill);
+        if ((stack <= 0 && spill <= 0) || getenv("PERM_ALLOW_SPILL")) { b.ok = true; break; }  // knob: experiments only
         // escalate: larger register cap, then a shorter unrolled block, then fewer chunk bits
         if (b.sp.min_blocks > 1) b.sp.min_blocks -= 1;
         else if (b.sp.U > 2) b.sp.U -= 1;
@@ -686,6 +812,9 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       I.nvrtc_ms += b.nvrtc_ms;
       if (!b.ok) continue;
       const double score = (n == 1 || p->singular) ? 0.0 : b.kc.w_plan / eff(bps_of(b.regs, b.sp.threads));
+      if (dbg_plan)
+        fprintf(stderr, "[plan] built K %d B %d U %d minb %d regs %d w %.5f score %.5f ok %d\n", c.K, b.sp.B,
+                b.sp.U, b.sp.min_blocks, b.regs, b.kc.w_plan, score, (int)b.ok);
       if (!have || score < best_score) {
         have = true;
         best_score = score;
@@ -729,6 +858,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     g_plan_cache[pkey] = *p;
   }
   I.plan_ms = now_ms() - t0;
+  if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] planning %.3f ms (cached %d)\n", I.plan_ms, I.plan_cached);
   if (!p->opts.no_device) {
     st = load_device(p);
     if (st != PERM_OK) return bail(st);
@@ -970,15 +1100,15 @@ void perm_free(perm_plan_t p) {
   if (p->on_device) {
     cudaSetDevice(p->device);
     if (p->stream) cudaStreamSynchronize(p->stream);
-    if (p->d_slots) cudaFree(p->d_slots);
-    if (p->d_counter) cudaFree(p->d_counter);
-    if (p->d_rscratch) cudaFree(p->d_rscratch);
-    if (p->d_partial) cudaFree(p->d_partial);
-    if (p->d_scratch) cudaFree(p->d_scratch);
-    if (p->d_tier) cudaFree(p->d_tier);
+    pool_free(p->device, p->d_slots, p->slots_bytes);
+    pool_free(p->device, p->d_counter, p->counter_bytes);
+    pool_free(p->device, p->d_rscratch, p->rscratch_bytes);
+    pool_free(p->device, p->d_partial, p->partial_bytes);
+    pool_free(p->device, p->d_scratch, p->scratch_bytes);
+    pool_free(p->device, p->d_tier, p->tier_alloc_bytes);
     for (auto& e : p->ev)
       if (e) cudaEventDestroy(e);
-    if (p->lib) cudaLibraryUnload(p->lib);
+    if (p->lib_held) lib_release(p->device, p->lib_key);
     if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   }
   delete p;

@@ -41,9 +41,10 @@ def main():
         t3 = time.perf_counter()
         v = sp.value()
         t4 = time.perf_counter()
+        plan_ms = P.info["plan_ms"]
         P.close()
         t5 = time.perf_counter()
-        rows.append((t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4, P.info["plan_ms"]))
+        rows.append((t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4, plan_ms))
     print("plan+load | buffers | enqueue | sweep+sync+D2H | free | (plan_ms)   [ms]")
     for r in rows[1:]:
         print(" | ".join(f"{1000 * x:8.3f}" for x in r[:5]), f"| {r[5]:.3f}")
