@@ -727,7 +727,10 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       for (const Cand& c : cands)
         fprintf(stderr, "[plan] cand score %.5f w %.5f base %d K %d var %d bcap %d est %d cc %d\n", c.score, c.w,
                 c.base, c.K, c.var, c.bcap, c.est, (int)c.cc);
-    if (cands.size() > 3) cands.resize(3);
+    {
+      const size_t ncomp = getenv("PERM_PLAN_COMPILES") ? (size_t)atoi(getenv("PERM_PLAN_COMPILES")) : 3;
+      if (cands.size() > ncomp) cands.resize(ncomp);
+    }
     if (p->singular || n == 1) cands.resize(std::min<size_t>(cands.size(), 1));
     // compile the top candidates (NVRTC, spill gate with escalation) and keep
     // the best by W_plan / eff(actual registers)
