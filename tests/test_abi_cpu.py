@@ -219,3 +219,51 @@ def test_plan_geometry_and_work_model():
     assert i["tasks"] & (i["tasks"] - 1) == 0       # power of two (sharding)
     assert i["w_plan"] < i["w_alg1"]
     assert sorted(i["row_perm"]) == list(range(n)) and sorted(i["col_perm"]) == list(range(n))
+
+
+def _sass_dp_count(cubin: bytes) -> int:
+    with tempfile.NamedTemporaryFile(suffix=".cubin") as f:
+        f.write(cubin)
+        f.flush()
+        sass = subprocess.run(["cuobjdump", "-sass", f.name], capture_output=True, text=True).stdout
+    return len(re.findall(r"\bD(ADD|MUL|FMA)\b", sass))
+
+
+@pytest.mark.parametrize("n,p,seed", [(30, 0.3, 1), (40, 0.2, 1)])
+def test_post_pass_removes_dead_registers_and_contracts(n, p, seed):
+    """DESIGN 3.13: every loop-carried register the generated kernel declares is
+    read somewhere; single-use products feeding an add/sub become DFMAs; the
+    contraction lowers W_plan and the static DP instruction count."""
+    A = synth.erdos_renyi(n, p, seed)
+    P = pb.Plan.from_dense(A, mode="reg", no_device=True)
+    src = P.source
+    decls = re.findall(r"^\s*double (\w+) = ", src, re.M)
+    for r in decls:
+        if r in ("cacc", "lacc"):
+            continue
+        uses = len(re.findall(rf"\b{r}\b", src))
+        defs = 1 + len(re.findall(rf"^\s*{r} = ", src, re.M))
+        assert uses > defs, f"register {r} is never read"
+    assert re.search(r"= fma\(-?[\w(][^,]*, [^,]+, -", src), "no contracted a*b - c"
+    os.environ["PERM_NO_FUSE"] = "1"
+    try:
+        Q = pb.Plan.from_dense(A, mode="reg", no_device=True, factor_cols=P.info["K"] or -1,
+                               chunk_log2=P.info["B"], block_log2=P.info["U"])
+    finally:
+        del os.environ["PERM_NO_FUSE"]
+    if Q.info["K"] == P.info["K"] and Q.info["col_perm"] == P.info["col_perm"]:
+        assert P.info["w_plan"] < Q.info["w_plan"]
+        if shutil.which("cuobjdump"):
+            assert _sass_dp_count(P.cubin()) < _sass_dp_count(Q.cubin())
+
+
+def test_int01_codegen_uses_narrow_integer_types():
+    """DESIGN 3.9: INT01 products run in int / i64 where a magnitude bound
+    allows; only the accumulation path needs wrapping u128."""
+    B = synth.erdos_renyi(30, 0.25, 2, binary=True)
+    P = pb.Plan.from_dense(B, mode="int01", no_device=True)
+    src = P.source
+    assert P.info["local_bytes"] == 0
+    muls = re.findall(r"const (int|i64|u128) t\d+ = .*\*", src)
+    narrow = sum(1 for t in muls if t != "u128")
+    assert narrow > 0.3 * len(muls), (narrow, len(muls))

@@ -388,3 +388,41 @@ def test_complex_boson_sampling_band44():
     U = synth.unitary_brickwork(44, 4, 1)
     exp = oracle.perm_band_complex(U, synth.half_bandwidth(U))
     assert crel(plan(U).compute(), exp) < REL
+
+
+# ---- INT01 bound-typed integers at full size; runtime resource reuse -----------
+
+@pytest.mark.slow
+def test_int01_band44_bit_exact_vs_band_dp():
+    """INT01 (int / i64 / u128 typed by bounds, DESIGN 3.9) at n=44 against the
+    exact band DP of Eq. 1."""
+    B = (synth.givens_brickwork(44, 4, 1) != 0).astype(float)
+    w = synth.half_bandwidth(B)
+    P = plan(B, mode="int01")
+    assert P.exact() == oracle.perm_band_exact(B, w)
+
+
+def test_int01_typed_products_vs_fp64_path():
+    """0/1 ER n=30: INT01 exact result equals the exact doubled-integer NW oracle
+    and rounds to the FP64 sweep within the FP64 bar."""
+    B = synth.erdos_renyi(30, 0.25, 7, binary=True)
+    e = plan(B, mode="int01").exact()
+    assert e == oracle.perm_nw_exact(B)
+    assert rel(plan(B, mode="reg").compute(), float(e)) < REL
+
+
+def test_plans_share_cached_library_and_pooled_buffers():
+    """Re-planning the same matrix reuses the loaded library and recycled
+    buffers (DESIGN 3.14): results stay bitwise identical across plan/free
+    cycles and with two live plans sharing one library."""
+    A = synth.erdos_renyi(30, 0.25, 3)
+    ref = plan(A).compute()
+    P1 = plan(A)
+    P2 = plan(A)
+    assert P1.compute() == ref and P2.compute() == ref
+    P1.close()
+    assert P2.compute() == ref
+    for _ in range(3):
+        with plan(A) as P:
+            assert P.compute() == ref
+    P2.close()
