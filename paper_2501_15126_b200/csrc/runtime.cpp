@@ -103,6 +103,50 @@ void parse_ptxas(const std::string& log, int& regs, int& stack, int& spill) {
   }
 }
 
+// Register count and stack frame of the kernel from the cubin itself (the
+// .nv.info section's EIATTR_REGCOUNT / EIATTR_FRAME_SIZE entries).  NVRTC 12.9
+// serves repeated compiles from the driver's cache without running ptxas, so
+// the `-v` log can be empty on a GPU host: the spill gate must not depend on it.
+bool cubin_attrs(const std::vector<char>& cub, int& regs, int& frame) {
+  regs = frame = -1;
+  auto rd = [&](size_t off, size_t n) -> uint64_t {
+    uint64_t v = 0;
+    if (off + n > cub.size()) return 0;
+    std::memcpy(&v, cub.data() + off, n);
+    return v;
+  };
+  if (cub.size() < 64 || std::memcmp(cub.data(), "\x7f" "ELF", 4) != 0 || cub[4] != 2) return false;
+  const uint64_t shoff = rd(0x28, 8);
+  const uint64_t shentsize = rd(0x3a, 2), shnum = rd(0x3c, 2), shstrndx = rd(0x3e, 2);
+  if (shentsize < 64 || shstrndx >= shnum) return false;
+  auto sh = [&](uint64_t i, size_t field, size_t n) { return rd(shoff + i * shentsize + field, n); };
+  const uint64_t stroff = sh(shstrndx, 0x18, 8);
+  for (uint64_t i = 0; i < shnum; ++i) {
+    const uint64_t name = sh(i, 0, 4);
+    if (stroff + name + 9 > cub.size() || std::strcmp(cub.data() + stroff + name, ".nv.info") != 0) continue;
+    const uint64_t off = sh(i, 0x18, 8), size = sh(i, 0x20, 8);
+    for (uint64_t q = off; q + 2 <= off + size && q + 2 <= cub.size();) {
+      const int fmt = (unsigned char)cub[q], attr = (unsigned char)cub[q + 1];
+      if (fmt == 0x04) {  // EIFMT_SVAL: u16 size, payload (u32 symbol, u32 value for these)
+        const uint64_t len = rd(q + 2, 2);
+        if (len >= 8) {
+          const int val = (int)rd(q + 8, 4);
+          if (attr == 0x2f) regs = std::max(regs, val);    // EIATTR_REGCOUNT
+          if (attr == 0x11) frame = std::max(frame, val);  // EIATTR_FRAME_SIZE
+        }
+        q += 4 + len;
+      } else if (fmt == 0x03) {
+        q += 4;  // EIFMT_HVAL
+      } else if (fmt == 0x02) {
+        q += 4;  // EIFMT_BVAL (padded)
+      } else {
+        q += 2;  // EIFMT_NVAL
+      }
+    }
+  }
+  return regs >= 0;
+}
+
 bool all_ones(const Csx& a) {
   for (double v : a.val)
     if (v != 1.0) return false;
@@ -778,6 +822,14 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         if (b.status != PERM_OK) { b.err = g_err; return b; }
         b.nvrtc_ms += ms;
         parse_ptxas(b.log, b.regs, stack, spill);
+        {  // authoritative: the cubin's own attributes (the log may be empty, see cubin_attrs)
+          int cr = -1, cf = -1;
+          if (cubin_attrs(b.cubin, cr, cf)) {
+            b.regs = cr;
+            stack = std::max(stack, cf);
+            if (cf > 0) spill = std::max(spill, cf);
+          }
+        }
         if (getenv("PERM_DEBUG_PLAN"))
           fprintf(stderr, "[plan]   attempt K %d B %d U %d minb %d cc %d: regs %d stack %d spill %d\n", c.K, b.sp.B,
                   b.sp.U, b.sp.min_blocks, (int)b.sp.cc, b.regs, stack, spill);

@@ -151,6 +151,15 @@ def test_codegen_compiles_without_spills(n, p, seed, mode):
             sass = subprocess.run(["cuobjdump", "-sass", f.name], capture_output=True, text=True).stdout
         assert "sm_100a" in sass
         assert not re.search(r"\b(LDL|STL)\b", sass), "local memory in generated kernel"
+        with tempfile.NamedTemporaryFile(suffix=".cubin") as f:
+            f.write(cub)
+            f.flush()
+            elf = subprocess.run(["cuobjdump", "-elf", f.name], capture_output=True, text=True).stdout
+        # the planner reads registers / frame from the cubin's .nv.info (not the ptxas log)
+        m = re.search(r"register count: (\d+)", elf)
+        assert m and int(m.group(1)) == i["regs_per_thread"]
+        fr = re.search(r"frame size: (0x[0-9a-f]+)", elf)
+        assert fr is None or int(fr.group(1), 16) == 0
         if mode != "int01":
             assert re.search(r"\bD(ADD|MUL|FMA)\b", sass)
 
