@@ -666,7 +666,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       const int r8 = (std::max(regs, 16) + 7) / 8 * 8;
       return std::max(1, std::min(16, 65536 / (threads * r8)));
     };
-    struct Cand { double score, w; int base, K, var, bcap, est; bool cc; };
+    struct Cand { double score, w; int base, K, var, bcap, est; bool cc; int ev; };
     // composite caches (DESIGN 3.12): candidates with and without
     const bool cc_allowed = !(getenv("PERM_NO_CC") && atoi(getenv("PERM_NO_CC")) == 1);
     std::vector<Cand> cands;
@@ -685,19 +685,33 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     // complex values take 4 registers: halve the composite size bound
     const int elim_maxsize = getenv("PERM_ELIM_MAXSIZE") ? atoi(getenv("PERM_ELIM_MAXSIZE"))
                                                          : (mode == PERM_MODE_COMPLEX_INTERNAL ? 40 : 96);
-    const int elim_beam = std::max(1, getenv("PERM_ELIM_BEAM") ? atoi(getenv("PERM_ELIM_BEAM")) : 1);
-    auto greedy_elim = [&](const std::vector<int>& rp, const std::vector<int>& cp) {
+    // beam width of the elimination searches (FP64: 4, INT01 / complex: greedy)
+    const int elim_beam = std::max(1, getenv("PERM_ELIM_BEAM") ? atoi(getenv("PERM_ELIM_BEAM"))
+                                      : ((mode == PERM_MODE_REG || mode == PERM_MODE_HYBRID) ? 4 : 1));
+    // ev % 3: how the search scores a sequence -- 0: the kernel as planned
+    // (U <= 4); 1: with Alg. 4's register/global split applied (FP64 only);
+    // 2: U <= 3.  ev / 3: greedy or beam search.  The W landscape is rugged (a
+    // greedy path can end far from the best, and a beam is not a superset of
+    // the greedy path), so the sequences of every search become candidates.
+    auto greedy_elim = [&](const std::vector<int>& rp, const std::vector<int>& cp, int ev) {
       std::vector<int> seq;
       if (kcap == 0) return seq;
-      auto evalW = [&](const std::vector<int>& s) {
+      auto evalW = [&, ev](const std::vector<int>& s) {
         const int k = (int)s.size();
         std::vector<int> c = costsort_swept(p->ccs, factored_columns(cp, s, k), k);
         Csx o = permute_ccs(p->ccs, rp, c);
         KernelSpec sp;
         geometry(k, sp, 8);
-        sp.U = std::min(sp.U, 4);
+        const int sc = ev % 3;  // scoring; ev / 3: greedy (0) or beam (1)
+        sp.U = std::min(sp.U, sc == 2 ? 3 : 4);
         sp.cc = cc_allowed;
         set_hybrid(sp, o);
+        if (sc == 1 && (mode == PERM_MODE_REG || mode == PERM_MODE_HYBRID)) {
+          int k4, c4;
+          partition_alg4(o, gr, 148, k4, c4);
+          sp.mode = PERM_MODE_HYBRID;
+          sp.hybrid_c = std::max(std::min(c4 - k, sp.B), std::min(sp.U, sp.B));
+        }
         return generate_kernel(o, make_x0(o), sp).w_plan;
       };
       // beam search (width 1 = greedy) over elimination sequences
@@ -732,19 +746,42 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         std::sort(next.begin(), next.end());
         if (!(next[0].first < best.first * 0.995)) break;  // no further gain
         best = next[0];
-        if ((int)next.size() > elim_beam) next.resize(elim_beam);
+        const int width = ev >= 3 ? elim_beam : 1;
+        if ((int)next.size() > width) next.resize(width);
         beam.swap(next);
       }
       return best.second;
     };
-    std::map<int, std::vector<int>> elim_of_base;
-    for (int base : bases) {
+    std::map<int, std::vector<int>> elim_of_base;  // key: base * 8 + ev
+    const bool fp64 = mode == PERM_MODE_REG || mode == PERM_MODE_HYBRID;
+    // ev = scoring (ev % 3) x search (ev / 3: greedy, beam of width elim_beam)
+    const int nev = getenv("PERM_ELIM_VARIANTS") ? std::max(1, atoi(getenv("PERM_ELIM_VARIANTS")))
+                                                 : (fp64 ? (elim_beam > 1 ? 6 : 3) : 3);
+    {
+      std::vector<std::pair<int, std::future<std::vector<int>>>> runs;  // greedy runs, concurrently
+      for (int base : bases)
+        for (int ev = 0; ev < nev; ++ev) {
+          if (ev % 3 == 1 && !fp64) continue;
+          runs.emplace_back(base * 8 + ev, std::async(std::launch::async, [&, base, ev] {
+                              std::vector<int> rp, cp;
+                              order_with(base, rp, cp);
+                              return greedy_elim(rp, cp, ev);
+                            }));
+        }
+      for (auto& r : runs) elim_of_base[r.first] = r.second.get();
+    }
+    for (auto& be : elim_of_base) {
+      const int base = be.first / 8, ev = be.first % 8;
+      const std::vector<int>& picks = be.second;
+      bool dup = false;  // the same sequence found under another scoring
+      for (auto& o2 : elim_of_base)
+        if (o2.first < be.first && o2.first / 8 == base && o2.second == picks) dup = true;
+      if (dup) continue;
       std::vector<int> rp, cp;
       order_with(base, rp, cp);
-      std::vector<int> picks = greedy_elim(rp, cp);
-      elim_of_base[base] = picks;
       const int kmax = (int)picks.size();
-      for (int K = (p->opts.factor_cols > 0 ? kmax : 0); K <= kmax; ++K)
+      const int kmin = p->opts.factor_cols > 0 ? kmax : (ev == 0 ? 0 : std::max(0, kmax - 2));
+      for (int K = kmin; K <= kmax; ++K)
         for (int var = 0; var < nvar; ++var) {
           Csx o = permute_ccs(p->ccs, rp, colp_of(cp, picks, K, var));
           std::vector<double> xo = make_x0(o);
@@ -760,7 +797,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
               // estimates above the 255-register cap are optimistic-capped: ptxas
               // usually fits them (2 blocks of 128); the spill gate escalates if not
               const double score = kc.w_plan / eff(bps_of(std::min(kc.est_regs, 255), sp.threads));
-              cands.push_back({score, kc.w_plan, base, K, var, bc, kc.est_regs, sp.cc});
+              cands.push_back({score, kc.w_plan, base, K, var, bc, kc.est_regs, sp.cc, ev});
             }
           }
         }
@@ -801,7 +838,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       Built b;
       std::vector<int> cp;
       order_with(c.base, b.rp, cp);
-      b.colp = colp_of(cp, elim_of_base[c.base], c.K, c.var);
+      b.colp = colp_of(cp, elim_of_base[c.base * 8 + c.ev], c.K, c.var);
       b.o = permute_ccs(p->ccs, b.rp, b.colp);
       b.xo = make_x0(b.o);
       b.tasks = geometry(c.K, b.sp, c.bcap);
