@@ -34,7 +34,7 @@ PAPER_STEPS_PER_S = (2 ** 39 - 1) / 3.94   # CodeGen-Hybrid, A100, n=40 p=0.2 (P
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dim", dest="n", type=int, default=N_DIM)
@@ -62,50 +62,78 @@ def workload(args):
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (recipe's clocks line)."""
+    """SM clock + throttle reasons sampled DURING the timed region (the
+    recipe's clocks line): NVML polled every 2 ms from a thread (an nvidia-smi
+    loop needs ~100 ms to start, longer than a short timed region), with one
+    sample right at entry and exit; nvidia-smi is the fallback."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
-        self.proc = None
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.stop = threading.Event()
+        self.nvml = None
+
+    def _sample(self):
+        nv, h = self.nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.samples.append((float(sm), float(mx), int(rs)))
+
+    def _loop(self):
+        while not self.stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            self.stop.wait(0.002)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml = (nv, nv.nvmlDeviceGetHandleByIndex(self.index))
+            self._sample()
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.nvml = None
+            self._smi()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.samples.append([s.strip() for s in line.split(",")])
+    def _smi(self):
+        try:
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10).stdout
+            f = [x.strip() for x in out.split(",")]
+            bits = [0x8, 0x40, 0x20, 0x4]
+            self.samples.append((float(f[0]), float(f[1]),
+                                 sum(b for b, v in zip(bits, f[2:6]) if v.lower() == "active")))
+        except Exception:
+            pass
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+        if self.nvml:
+            self.stop.set()
+            self.t.join(timeout=2)
             try:
-                self.proc.wait(timeout=5)
+                self._sample()
             except Exception:
-                self.proc.kill()
+                pass
+        else:
+            self._smi()
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if len(s) > 3 + k and s[3 + k].lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+        sm = sorted(s[0] for s in self.samples)
+        reasons = sorted({k for s in self.samples for k, b in self.REASONS.items() if s[2] & b})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def cpu_baseline(A, target_s: float):

@@ -30,5 +30,6 @@ def test_two_ranks_share_one_gpu_bitwise():
                "--backend", "gloo", "--same-device", *common])
     assert one["n_gpus"] == 1 and two["n_gpus"] == 2
     assert two["result"] == one["result"]
-    assert two["gpu_launches"] == one["gpu_launches"]
+    # per step: sweep + tree passes over the rank's slots + fold (fewer passes per shard)
+    assert 0 < two["gpu_launches"] <= one["gpu_launches"]
     assert two["value"] > 0 and two["e2e"]["value"] > 0
