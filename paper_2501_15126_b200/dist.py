@@ -20,6 +20,16 @@ class ShardedPermanent:
         self.part = torch.zeros(2, dtype=torch.float64, device=device)
         self.gathered = torch.zeros(2 * world, dtype=torch.float64, device=device)
         self.out = torch.zeros(2, dtype=torch.float64, device=device)
+        if world > 1:
+            # every rank plans on its own: the shards only form one reduction
+            # tree if all ranks chose the same plan (ordering, K, geometry)
+            import torch.distributed as dist
+            i = plan.info
+            sig = (i["K"], i["B"], i["U"], i["M"], i["tasks"], tuple(i["col_perm"]), tuple(i["row_perm"]))
+            sigs = [None] * world
+            dist.all_gather_object(sigs, sig, group=group)
+            if any(s != sigs[0] for s in sigs):
+                raise RuntimeError(f"ranks planned different kernels: {sigs}")
 
     def step(self):
         """Enqueue shard sweep + all-gather + fold on the current stream."""
