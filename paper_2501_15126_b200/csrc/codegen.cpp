@@ -1221,6 +1221,10 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
                      ") : " + (g.has_frozen ? P : std::string("cplx{1.0, 0.0}")) + ";");
     else g.line("cacc = (chunk & 1ull) ? (" + std::string(g.PT()) + ")(0 - " + P + ") : " + P + ";");
   } else {
+    // INT01 zero tracking at chunk level: the frozen product F is constant over
+    // the chunk, so a warp whose 32 lanes all have F == 0 skips the chunk
+    const bool chunk_skip = g.zs && g.has_frozen;
+    if (chunk_skip) g.line("if (!__all_sync(0xffffffffu, F == 0)) {");
     // the signs need only bits U..B of h = (chunk << B) | (blk << U): bits
     // U..B-1 are blk, bit B is chunk bit 0 (= lane bit 0); a 32-bit hu keeps
     // the 64-bit h0 out of the loop (registers)
@@ -1271,6 +1275,7 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
     ops_body = g.ops;
     g.ind = "      ";
     g.line("}");
+    if (chunk_skip) g.line("}");
   }
   const std::string acc_stmt = g.cx ? "lacc = cadd(lacc, cacc);" : "lacc += cacc;";
   if (masked) g.line("if (chunk < " + std::to_string(S.nchunks_total) + "ull) " + acc_stmt);

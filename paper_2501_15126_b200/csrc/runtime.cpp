@@ -666,14 +666,70 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       const int r8 = (std::max(regs, 16) + 7) / 8 * 8;
       return std::max(1, std::min(16, 65536 / (threads * r8)));
     };
-    struct Cand { double score, w; int base, K, var, bcap, est; bool cc; int ev; };
+    struct Cand { double score, w; int base, K, var, bcap, est; bool cc; int ev; double pskip; };
     // composite caches (DESIGN 3.12): candidates with and without
     const bool cc_allowed = !(getenv("PERM_NO_CC") && atoi(getenv("PERM_NO_CC")) == 1);
     std::vector<Cand> cands;
     // swept-column variants: 0 = base order, 1 = sorted by flip cost (AUTO only)
     const int nvar = ord == PERM_ORDER_AUTO ? 2 : 1;
-    auto colp_of = [&](const std::vector<int>& cp, const std::vector<int>& picks, int K, int var) {
+    // INT01 zero tracking at warp-task level (extends Sec. VI-B): the
+    // columns of a few even-degree plain rows go to the top swept positions
+    // (bits >= B + 5, uniform over the 32 lanes of a warp-task), so those rows
+    // are frozen and lane-uniform; whenever one of them is 0 (2y_r = sum of
+    // +-1 over its columns balances), F == 0 on every lane and the warp skips
+    // the chunk (generated `__all_sync(F == 0)`).  Returns the order and the
+    // skipped fraction of chunks 1 - prod_r (1 - P(row r is 0)).
+    std::vector<std::vector<int>> row_cols(n);
+    for (int j = 0; j < n; ++j)
+      for (int q = p->ccs.ptr[j]; q < p->ccs.ptr[j + 1]; ++q) row_cols[p->ccs.idx[q]].push_back(j);
+    auto zero_aware = [&](const std::vector<int>& colp, int K, int B, double& pskip) {
+      pskip = 0;
+      const int top = (n - 1 - K) - B - 5;
+      if (top < 1) return colp;
+      const int last = colp[n - 1];
+      std::set<int> elim(colp.begin(), colp.begin() + K);
+      struct R { double pz; int r; };
+      std::vector<R> rows;
+      for (int r = 0; r < n; ++r) {
+        const int d = (int)row_cols[r].size();
+        if (d < 2 || (d & 1)) continue;
+        bool ok = true, has_last = false;
+        for (int c : row_cols[r]) { ok &= !elim.count(c); has_last |= c == last; }
+        if (!ok) continue;
+        // P(sum of the swept signs = -(last column's +1)) or P(sum = 0)
+        const int m = has_last ? d - 1 : d, need = has_last ? d / 2 - 1 : d / 2;
+        const double pz = std::exp(std::lgamma(m + 1.0) - std::lgamma(need + 1.0) - std::lgamma(m - need + 1.0) -
+                                   m * std::log(2.0));
+        rows.push_back({pz, r});
+      }
+      std::stable_sort(rows.begin(), rows.end(), [](const R& a, const R& b) { return a.pz > b.pz; });
+      std::set<int> chosen_cols;
+      double keep = 1.0;
+      for (const R& x : rows) {
+        std::set<int> u = chosen_cols;
+        for (int c : row_cols[x.r]) if (c != last) u.insert(c);
+        if ((int)u.size() > top) continue;
+        chosen_cols.swap(u);
+        keep *= 1.0 - x.pz;
+      }
+      if (chosen_cols.empty()) return colp;
+      pskip = 1.0 - keep;
+      std::vector<int> out(colp.begin(), colp.begin() + K), hi;
+      for (int q = K; q < n - 1; ++q) (chosen_cols.count(colp[q]) ? hi : out).push_back(colp[q]);
+      out.insert(out.end(), hi.begin(), hi.end());
+      out.push_back(last);
+      return out;
+    };
+    auto colp_of = [&](const std::vector<int>& cp, const std::vector<int>& picks, int K, int var, int B = 0,
+                       double* pskip = nullptr) {
       std::vector<int> c = factored_columns(cp, picks, K);
+      if (var == 2) {  // zero-aware placement on top of the cost-sorted order (INT01)
+        c = costsort_swept(p->ccs, c, K);
+        double ps = 0;
+        c = zero_aware(c, K, B, ps);
+        if (pskip) *pskip = ps;
+        return c;
+      }
       return var ? costsort_swept(p->ccs, c, K) : c;
     };
     // Elimination sequence per base ordering: greedy, each step
@@ -782,8 +838,9 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       const int kmax = (int)picks.size();
       const int kmin = p->opts.factor_cols > 0 ? kmax : (ev == 0 ? 0 : std::max(0, kmax - 2));
       for (int K = kmin; K <= kmax; ++K)
-        for (int var = 0; var < nvar; ++var) {
-          Csx o = permute_ccs(p->ccs, rp, colp_of(cp, picks, K, var));
+        for (int var = 0; var < nvar + (mode == PERM_MODE_INT01 ? 1 : 0); ++var) {
+          const int vv = var < nvar ? var : 2;
+          Csx o = permute_ccs(p->ccs, rp, colp_of(cp, picks, K, vv));
           std::vector<double> xo = make_x0(o);
           std::set<int> seenB;
           for (int bc : bcaps) {
@@ -791,13 +848,20 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
             geometry(K, sp, bc);
             set_hybrid(sp, o);
             if (!seenB.insert(sp.B).second) continue;  // cap not binding: duplicate
+            double pskip = 0;
+            if (vv == 2) {  // the placement depends on B
+              o = permute_ccs(p->ccs, rp, colp_of(cp, picks, K, 2, sp.B, &pskip));
+              xo = make_x0(o);
+              if (pskip <= 0) continue;
+            }
             for (int ccv = 0; ccv < (K > 0 && cc_allowed ? 2 : 1); ++ccv) {
               sp.cc = ccv == 1;
               KernelCode kc = generate_kernel(o, xo, sp);
               // estimates above the 255-register cap are optimistic-capped: ptxas
               // usually fits them (2 blocks of 128); the spill gate escalates if not
-              const double score = kc.w_plan / eff(bps_of(std::min(kc.est_regs, 255), sp.threads));
-              cands.push_back({score, kc.w_plan, base, K, var, bc, kc.est_regs, sp.cc, ev});
+              const double score =
+                  kc.w_plan * (1.0 - pskip) / eff(bps_of(std::min(kc.est_regs, 255), sp.threads));
+              cands.push_back({score, kc.w_plan, base, K, vv, bc, kc.est_regs, sp.cc, ev, pskip});
             }
           }
         }
@@ -806,8 +870,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     const bool dbg_plan = getenv("PERM_DEBUG_PLAN") != nullptr;
     if (dbg_plan)
       for (const Cand& c : cands)
-        fprintf(stderr, "[plan] cand score %.5f w %.5f base %d K %d var %d bcap %d est %d cc %d\n", c.score, c.w,
-                c.base, c.K, c.var, c.bcap, c.est, (int)c.cc);
+        fprintf(stderr, "[plan] cand score %.5f w %.5f base %d K %d var %d bcap %d est %d cc %d pskip %.3f\n", c.score, c.w,
+                c.base, c.K, c.var, c.bcap, c.est, (int)c.cc, c.pskip);
     {
       const size_t ncomp = getenv("PERM_PLAN_COMPILES") ? (size_t)atoi(getenv("PERM_PLAN_COMPILES")) : 3;
       if (cands.size() > ncomp) cands.resize(ncomp);
@@ -838,10 +902,10 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       Built b;
       std::vector<int> cp;
       order_with(c.base, b.rp, cp);
-      b.colp = colp_of(cp, elim_of_base[c.base * 8 + c.ev], c.K, c.var);
+      b.tasks = geometry(c.K, b.sp, c.bcap);
+      b.colp = colp_of(cp, elim_of_base[c.base * 8 + c.ev], c.K, c.var, b.sp.B);
       b.o = permute_ccs(p->ccs, b.rp, b.colp);
       b.xo = make_x0(b.o);
-      b.tasks = geometry(c.K, b.sp, c.bcap);
       b.sp.cc = c.cc;
       set_hybrid(b.sp, b.o);
       if (n == 1 || p->singular) { b.ok = true; return b; }
@@ -891,6 +955,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         Cand plain = cands[ci];
         plain.K = 0;
         plain.var = 0;
+        plain.pskip = 0;
         cands.push_back(plain);
         fut.push_back(std::async(std::launch::async, build, plain));
       }
@@ -903,7 +968,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       }
       I.nvrtc_ms += b.nvrtc_ms;
       if (!b.ok) continue;
-      const double score = (n == 1 || p->singular) ? 0.0 : b.kc.w_plan / eff(bps_of(b.regs, b.sp.threads));
+      const double score =
+          (n == 1 || p->singular) ? 0.0 : b.kc.w_plan * (1.0 - c.pskip) / eff(bps_of(b.regs, b.sp.threads));
       if (dbg_plan)
         fprintf(stderr, "[plan] built K %d B %d U %d minb %d regs %d w %.5f score %.5f ok %d\n", c.K, b.sp.B,
                 b.sp.U, b.sp.min_blocks, b.regs, b.kc.w_plan, score, (int)b.ok);
