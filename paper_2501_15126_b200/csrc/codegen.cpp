@@ -1223,7 +1223,7 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
   } else {
     // INT01 zero tracking at chunk level: the frozen product F is constant over
     // the chunk, so a warp whose 32 lanes all have F == 0 skips the chunk
-    const bool chunk_skip = g.zs && g.has_frozen;
+    const bool chunk_skip = g.i01 && S.zero_skip && g.has_frozen;
     if (chunk_skip) g.line("if (!__all_sync(0xffffffffu, F == 0)) {");
     // the signs need only bits U..B of h = (chunk << B) | (blk << U): bits
     // U..B-1 are blk, bit B is chunk bit 0 (= lane bit 0); a 32-bit hu keeps

@@ -708,12 +708,51 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       for (const R& x : rows) {
         std::set<int> u = chosen_cols;
         for (int c : row_cols[x.r]) if (c != last) u.insert(c);
-        if ((int)u.size() > top) continue;
+        if ((int)u.size() > std::min(top, 31)) continue;
         chosen_cols.swap(u);
         keep *= 1.0 - x.pz;
       }
       if (chosen_cols.empty()) return colp;
-      pskip = 1.0 - keep;
+      (void)keep;  // rows sharing columns are correlated: count the skipped fraction exactly
+      {
+        std::vector<int> cols(chosen_cols.begin(), chosen_cols.end());
+        const int c = (int)cols.size();
+        std::map<int, int> bit;
+        for (int q = 0; q < c; ++q) bit[cols[q]] = q;
+        std::vector<std::pair<uint32_t, int>> rm;  // (mask over chosen columns, +1 signs needed)
+        for (const R& x : rows) {
+          uint32_t m = 0;
+          bool fits = true, has_last = false;
+          for (int col : row_cols[x.r]) {
+            if (col == last) { has_last = true; continue; }
+            auto it = bit.find(col);
+            if (it == bit.end()) { fits = false; break; }
+            m |= 1u << it->second;
+          }
+          if (!fits) continue;
+          const int d = __builtin_popcount(m) + (has_last ? 1 : 0);
+          rm.push_back({m, d / 2 - (has_last ? 1 : 0)});  // #(+1) among the swept columns for a zero sum
+        }
+        uint64_t hit = 0, tot = 0;
+        auto count = [&](uint32_t st) {
+          ++tot;
+          for (auto& q : rm)
+            if (__builtin_popcount(st & q.first) == q.second) { ++hit; return; }
+        };
+        if (c <= 20) {
+          for (uint32_t st = 0; st < (1u << c); ++st) count(st);
+        } else {  // SplitMix64 sample of the column states
+          uint64_t z = 0x9E3779B97F4A7C15ull;
+          for (int q = 0; q < (1 << 20); ++q) {
+            z += 0x9E3779B97F4A7C15ull;
+            uint64_t v = z;
+            v = (v ^ (v >> 30)) * 0xBF58476D1CE4E5B9ull;
+            v = (v ^ (v >> 27)) * 0x94D049BB133111EBull;
+            count((uint32_t)(v ^ (v >> 31)));
+          }
+        }
+        pskip = tot ? (double)hit / (double)tot : 0.0;
+      }
       std::vector<int> out(colp.begin(), colp.begin() + K), hi;
       for (int q = K; q < n - 1; ++q) (chosen_cols.count(colp[q]) ? hi : out).push_back(colp[q]);
       out.insert(out.end(), hi.begin(), hi.end());
@@ -838,7 +877,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       const int kmax = (int)picks.size();
       const int kmin = p->opts.factor_cols > 0 ? kmax : (ev == 0 ? 0 : std::max(0, kmax - 2));
       for (int K = kmin; K <= kmax; ++K)
-        for (int var = 0; var < nvar + (mode == PERM_MODE_INT01 ? 1 : 0); ++var) {
+        for (int var = 0; var < nvar + (mode == PERM_MODE_INT01 && p->opts.zero_skip >= 0 ? 1 : 0); ++var) {
           const int vv = var < nvar ? var : 2;
           Csx o = permute_ccs(p->ccs, rp, colp_of(cp, picks, K, vv));
           std::vector<double> xo = make_x0(o);
