@@ -276,3 +276,15 @@ def test_int01_codegen_uses_narrow_integer_types():
     muls = re.findall(r"const (int|i64|u128) t\d+ = .*\*", src)
     narrow = sum(1 for t in muls if t != "u128")
     assert narrow > 0.3 * len(muls), (narrow, len(muls))
+
+
+def test_int01_zero_aware_placement_is_chosen_for_binary_er():
+    """0/1 ER n=40 p=0.2: the planner puts even-degree rows' columns on
+    lane-uniform bits (swept order 2) and the kernel skips chunks whose frozen
+    product is 0 on all 32 lanes."""
+    B = synth.erdos_renyi(40, 0.2, 1, binary=True)
+    P = pb.Plan.from_dense(B, mode="int01", no_device=True)
+    i = P.info
+    assert i["swept_order"] == 2 and i["seed_rows"] > 0
+    assert "__all_sync(0xffffffffu, F == 0)" in P.source
+    assert sorted(i["col_perm"]) == list(range(40))

@@ -426,3 +426,15 @@ def test_plans_share_cached_library_and_pooled_buffers():
         with plan(A) as P:
             assert P.compute() == ref
     P2.close()
+
+
+@pytest.mark.parametrize("n,seed", [(32, 1), (32, 2), (34, 3)])
+def test_int01_zero_aware_warp_skip_bit_exact(n, seed):
+    """INT01 warp-task zero skip (DESIGN 3.9): whichever placement the planner
+    picks, the result is the exact permanent; with the zero-aware placement the
+    kernel carries the lane-uniform chunk skip."""
+    B = synth.erdos_renyi(n, 0.2, seed, binary=True)
+    P = plan(B, mode="int01")
+    if P.info["swept_order"] == 2:
+        assert "__all_sync(0xffffffffu, F == 0)" in P.source
+    assert P.exact() == oracle.perm_nw_exact(B)
