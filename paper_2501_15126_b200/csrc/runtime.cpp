@@ -782,7 +782,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
                                                          : (mode == PERM_MODE_COMPLEX_INTERNAL ? 40 : 96);
     // beam width of the elimination searches (FP64: 4, INT01 / complex: greedy)
     const int elim_beam = std::max(1, getenv("PERM_ELIM_BEAM") ? atoi(getenv("PERM_ELIM_BEAM"))
-                                      : (mode == PERM_MODE_COMPLEX_INTERNAL ? 1 : 4));
+                                      : ((mode == PERM_MODE_REG || mode == PERM_MODE_HYBRID) ? 4 : 1));
     // ev % 3: how the search scores a sequence -- 0: the kernel as planned
     // (U <= 4); 1: with Alg. 4's register/global split applied (FP64 only);
     // 2: U <= 3.  ev / 3: greedy or beam search.  The W landscape is rugged (a
