@@ -782,7 +782,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
                                                          : (mode == PERM_MODE_COMPLEX_INTERNAL ? 40 : 96);
     // beam width of the elimination searches (FP64: 4, INT01 / complex: greedy)
     const int elim_beam = std::max(1, getenv("PERM_ELIM_BEAM") ? atoi(getenv("PERM_ELIM_BEAM"))
-                                      : ((mode == PERM_MODE_REG || mode == PERM_MODE_HYBRID) ? 4 : 1));
+                                      : (mode == PERM_MODE_COMPLEX_INTERNAL ? 1 : 4));
     // ev % 3: how the search scores a sequence -- 0: the kernel as planned
     // (U <= 4); 1: with Alg. 4's register/global split applied (FP64 only);
     // 2: U <= 3.  ev / 3: greedy or beam search.  The W landscape is rugged (a
@@ -912,13 +912,12 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         fprintf(stderr, "[plan] cand score %.5f w %.5f base %d K %d var %d bcap %d est %d cc %d pskip %.3f\n", c.score, c.w,
                 c.base, c.K, c.var, c.bcap, c.est, (int)c.cc, c.pskip);
     {
-      const size_t ncomp = getenv("PERM_PLAN_COMPILES") ? (size_t)atoi(getenv("PERM_PLAN_COMPILES")) : 3;
+      const size_t ncomp = getenv("PERM_PLAN_COMPILES") ? (size_t)atoi(getenv("PERM_PLAN_COMPILES")) : 4;
       if (cands.size() > ncomp) cands.resize(ncomp);
     }
     if (p->singular || n == 1) cands.resize(std::min<size_t>(cands.size(), 1));
     // compile the top candidates (NVRTC, spill gate with escalation) and keep
     // the best by W_plan / eff(actual registers)
-    double best_score = 1e300;
     bool have = false;
     struct Built {
       int status = PERM_OK;
@@ -935,6 +934,94 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       int regs = -1;
       double nvrtc_ms = 0;
       bool cached = false;
+    };
+    // measured seconds per Gray step of each compiled candidate on `device`: a
+    // few spread samples of its task range (zero skipping depends on the high
+    // task bits), four waves of warp-tasks each; candidates are timed in
+    // interleaved rounds after a warm-up (clock ramp) and the minimum over the
+    // rounds is kept; < 0 on any CUDA error
+    struct Timed {
+      cudaLibrary_t lib = nullptr;
+      cudaKernel_t k = nullptr;
+      void *d_cnt = nullptr, *d_slots = nullptr, *d_tier = nullptr;
+      uint64_t cnt = 0;
+      int S = 0;
+      unsigned grid = 0;
+      bool ok = false;
+    };
+    auto time_candidates = [&](const std::vector<const Built*>& bs, int device, bool wide) {
+      std::vector<double> out(bs.size(), -1.0);
+      std::vector<Timed> T(bs.size());
+      cudaStream_t st = nullptr;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      int sms = 0;
+      if (cudaSetDevice(device) != cudaSuccess ||
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+          cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+        cudaGetLastError();
+        return out;
+      }
+      for (size_t q = 0; q < bs.size(); ++q) {
+        const Built& b = *bs[q];
+        Timed& t = T[q];
+        int bps = 0;
+        if (b.tasks == 0 || b.cubin.empty()) continue;
+        if (cudaLibraryLoadData(&t.lib, b.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+            cudaLibraryGetKernel(&t.k, t.lib, b.kc.name.c_str()) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void*)t.k, b.sp.threads, 0) != cudaSuccess ||
+            bps < 1)
+          continue;
+        const uint64_t grid = (uint64_t)bps * sms, warps = grid * b.sp.threads / 32;
+        t.cnt = std::min<uint64_t>(b.tasks, 4 * warps);
+        t.S = (int)std::min<uint64_t>(4, b.tasks / t.cnt);
+        t.grid = (unsigned)std::min<uint64_t>(grid, (t.cnt * 32 + b.sp.threads - 1) / b.sp.threads);
+        if (cudaMalloc(&t.d_cnt, 256) != cudaSuccess || cudaMalloc(&t.d_slots, t.cnt * (wide ? 16 : 8)) != cudaSuccess)
+          continue;
+        if (b.kc.tier_bytes > 0 &&
+            cudaMalloc(&t.d_tier, (size_t)b.kc.tier_bytes * grid * b.sp.threads) != cudaSuccess)
+          continue;
+        t.ok = true;
+      }
+      auto launch = [&](size_t q, uint64_t first) {
+        const Built& b = *bs[q];
+        Timed& t = T[q];
+        unsigned long long tb = first;
+        unsigned tc = (unsigned)t.cnt;
+        void* args[] = {&tb, &tc, &t.d_cnt, &t.d_slots, &t.d_tier};
+        cudaMemsetAsync(t.d_cnt, 0, 4, st);
+        return cudaLaunchKernel((const void*)t.k, dim3(t.grid), dim3(b.sp.threads), args, 0, st);
+      };
+      auto sample = [&](size_t q) -> double {  // seconds per Gray step of one round
+        const Built& b = *bs[q];
+        Timed& t = T[q];
+        bool okl = cudaEventRecord(e0, st) == cudaSuccess;
+        for (int i = 0; i < t.S && okl; ++i) okl = launch(q, (b.tasks / t.S) * i / t.cnt * t.cnt) == cudaSuccess;
+        okl = okl && cudaEventRecord(e1, st) == cudaSuccess && cudaEventSynchronize(e1) == cudaSuccess;
+        float ms = 0;
+        if (!okl || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) return -1.0;
+        return ms * 1e-3 / ((double)t.S * t.cnt * 32.0 * b.sp.M * std::ldexp(1.0, b.sp.B + b.sp.K));
+      };
+      for (size_t q = 0; q < bs.size(); ++q)  // warm-up (module load, clock ramp)
+        if (T[q].ok && sample(q) < 0) T[q].ok = false;
+      for (int round = 0; round < 3; ++round)
+        for (size_t q = 0; q < bs.size(); ++q) {
+          if (!T[q].ok) continue;
+          const double v = sample(q);
+          if (v < 0) { T[q].ok = false; out[q] = -1.0; continue; }
+          out[q] = out[q] < 0 ? v : std::min(out[q], v);
+        }
+      cudaGetLastError();
+      for (Timed& t : T) {
+        if (t.d_cnt) cudaFree(t.d_cnt);
+        if (t.d_slots) cudaFree(t.d_slots);
+        if (t.d_tier) cudaFree(t.d_tier);
+        if (t.lib) cudaLibraryUnload(t.lib);
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      cudaStreamDestroy(st);
+      return out;
     };
     // one candidate: codegen + NVRTC with the spill gate and escalation
     auto build = [&](const Cand& c) {
@@ -986,10 +1073,12 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       }
       return b;
     };
+    struct Ok { double score; size_t ci; Built b; };
+    std::vector<Ok> oks;
     std::vector<std::future<Built>> fut;  // candidates compiled concurrently (NVRTC is thread-safe)
     for (const Cand& c : cands) fut.push_back(std::async(std::launch::async, build, c));
     for (size_t ci = 0; ci < cands.size(); ++ci) {
-      if (ci + 1 == cands.size() && !have && cands[ci].K > 0 && fut.size() == cands.size()) {
+      if (ci + 1 == cands.size() && oks.empty() && cands[ci].K > 0 && fut.size() == cands.size()) {
         // every elimination candidate spilled: fall back to the plain sweep (K = 0)
         Cand plain = cands[ci];
         plain.K = 0;
@@ -1012,16 +1101,41 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       if (dbg_plan)
         fprintf(stderr, "[plan] built K %d B %d U %d minb %d regs %d w %.5f score %.5f ok %d\n", c.K, b.sp.B,
                 b.sp.U, b.sp.min_blocks, b.regs, b.kc.w_plan, score, (int)b.ok);
-      if (!have || score < best_score) {
-        have = true;
-        best_score = score;
-        p->rowp = b.rp; p->colp = b.colp; p->occs = b.o; p->spec = b.sp; x0 = b.xo;
-        p->code = b.kc; p->cubin = b.cubin; p->ptxas_log = b.log;
-        I.ordering = c.base; I.tasks = b.tasks; I.K = c.K; I.swept_order = c.var;
-        I.regs_per_thread = b.regs;
-        I.local_bytes = 0;
-        I.cubin_cached = b.cached;
+      oks.push_back({score, ci, std::move(b)});
+    }
+    // model choice; then, with a device, measured choice (autotune): each
+    // compiled candidate sweeps a few spread samples of its task range, and
+    // replaces the model's pick only when it is clearly faster per Gray step
+    // (> 8 %), so near-ties stay deterministic across ranks
+    size_t pick = 0;
+    for (size_t q = 1; q < oks.size(); ++q)
+      if (oks[q].score < oks[pick].score) pick = q;
+    if (oks.size() > 1 && !p->opts.no_device && !(getenv("PERM_NO_AUTOTUNE") && atoi(getenv("PERM_NO_AUTOTUNE")))) {
+      std::vector<const Built*> bs;
+      for (const Ok& o : oks) bs.push_back(&o.b);
+      const std::vector<double> t = time_candidates(bs, p->opts.device, p->is_u128 || p->is_c128);
+      if (t[pick] > 0) {
+        size_t best = pick;
+        for (size_t q = 0; q < oks.size(); ++q)
+          if (t[q] > 0 && t[q] < t[best]) best = q;
+        if (best != pick && t[best] < 0.92 * t[pick]) pick = best;
       }
+      if (dbg_plan)
+        for (size_t q = 0; q < oks.size(); ++q)
+          fprintf(stderr, "[plan] autotune cand %zu: %.4g s per 2^30 Gray steps%s\n", q, t[q] * 1073741824.0,
+                  q == pick ? " <- pick" : "");
+    }
+    if (!oks.empty()) {
+      const Built& b = oks[pick].b;
+      const Cand& c = cands[oks[pick].ci];
+      have = true;
+
+      p->rowp = b.rp; p->colp = b.colp; p->occs = b.o; p->spec = b.sp; x0 = b.xo;
+      p->code = b.kc; p->cubin = b.cubin; p->ptxas_log = b.log;
+      I.ordering = c.base; I.tasks = b.tasks; I.K = c.K; I.swept_order = c.var;
+      I.regs_per_thread = b.regs;
+      I.local_bytes = 0;
+      I.cubin_cached = b.cached;
     }
     if (!have) {
       g_err = "every candidate kernel spills to local memory; reduce chunk_log2 or n";
