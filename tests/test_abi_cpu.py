@@ -172,8 +172,12 @@ def test_hybrid_codegen_uses_coalesced_tier():
     src = P.source
     assert "#define TIER(s) tier[(size_t)(s) * nt_ + gt_]" in src   # x[nthreads*row + tid], Listing 4
     assert "SG" in src                                              # cached tier product (globalProduct)
-    R = pb.Plan.from_dense(A, mode="reg", factor_cols=-1, no_device=True)
-    assert i["regs_per_thread"] < R.info["regs_per_thread"]
+    # same geometry and ordering: the tier takes rows out of the register file
+    geo = dict(factor_cols=-1, chunk_log2=i["B"], block_log2=i["U"], ordering=["none", "degree", "permanent"][i["ordering"]])
+    H = pb.Plan.from_dense(A, mode="hybrid", no_device=True, **geo)
+    R = pb.Plan.from_dense(A, mode="reg", no_device=True, **geo)
+    assert H.info["tier_rows"] > 0 and H.info["reg_rows"] < R.info["reg_rows"]
+    assert H.info["regs_per_thread"] <= R.info["regs_per_thread"]
 
 
 def test_codegen_literals_are_exact_hex():
