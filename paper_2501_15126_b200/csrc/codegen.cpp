@@ -1188,7 +1188,8 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
   // (the paper's coalesced x[nthreads * row + tid] layout, Listing 4)
   o << "#define TIER(s) tier[(size_t)(s) * nt_ + gt_]\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << S.threads << ", " << S.min_blocks << ")\n"
-    << kc.name << "(const u64 task_begin, const unsigned task_count, unsigned* __restrict__ counter, "
+    << kc.name << "(const u64 task_begin, const unsigned task_count, const u64 task_stride, "
+    << "unsigned* __restrict__ counter, "
     << g.PT() << "* __restrict__ slots, " << g.VT() << "* __restrict__ tier)\n{\n";
   g.ind = "  ";
   g.line("const unsigned lane = threadIdx.x & 31u;");
@@ -1202,7 +1203,7 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
   g.line("if (lane == 0) t = atomicAdd(counter, 1u);");
   g.line("t = __shfl_sync(0xffffffffu, t, 0);");
   g.line("if (t >= task_count) break;");
-  g.line("const u64 task = task_begin + t;");
+  g.line("const u64 task = task_begin + (u64)t * task_stride;  // stride 1 except planner samples");
   g.line(std::string(g.PT()) + " lacc = " + g.zero() + ";");
   g.line("#pragma unroll 1");
   g.line("for (unsigned m = 0; m < " + std::to_string(S.M) + "u; ++m) {");

@@ -388,7 +388,8 @@ int run_range(perm_plan_s* p, uint64_t first, uint64_t count, double* sweep_ms, 
   CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned), p->stream));
   unsigned long long tb = first;
   unsigned tc = (unsigned)count;
-  void* args[] = {&tb, &tc, &p->d_counter, &p->d_slots, &p->d_tier};
+  unsigned long long stride = 1;
+  void* args[] = {&tb, &tc, &stride, &p->d_counter, &p->d_slots, &p->d_tier};
   const int grid = (int)std::min<uint64_t>((uint64_t)p->info.grid,
                                            (count * 32 + p->spec.threads - 1) / p->spec.threads);
   CUDA_TRY(cudaEventRecord(p->ev[0], p->stream));
@@ -935,9 +936,9 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       double nvrtc_ms = 0;
       bool cached = false;
     };
-    // measured seconds per Gray step of each compiled candidate on `device`: a
-    // few spread samples of its task range (zero skipping depends on the high
-    // task bits), four waves of warp-tasks each; candidates are timed in
+    // measured seconds per Gray step of each compiled candidate on `device`:
+    // one launch over ~4 waves of warp-tasks strided across its whole task
+    // range (zero skipping depends on the high task bits); candidates are timed in
     // interleaved rounds after a warm-up (clock ramp) and the minimum over the
     // rounds is kept; < 0 on any CUDA error
     struct Timed {
@@ -973,8 +974,10 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
             bps < 1)
           continue;
         const uint64_t grid = (uint64_t)bps * sms, warps = grid * b.sp.threads / 32;
-        t.cnt = std::min<uint64_t>(b.tasks, 4 * warps);
-        t.S = (int)std::min<uint64_t>(4, b.tasks / t.cnt);
+        // one strided launch: tasks spread over the whole range (every task bit varies)
+        t.cnt = 1;
+        while (t.cnt * 2 <= std::min<uint64_t>(b.tasks, 4 * warps)) t.cnt *= 2;
+        t.S = 1;
         t.grid = (unsigned)std::min<uint64_t>(grid, (t.cnt * 32 + b.sp.threads - 1) / b.sp.threads);
         if (cudaMalloc(&t.d_cnt, 256) != cudaSuccess || cudaMalloc(&t.d_slots, t.cnt * (wide ? 16 : 8)) != cudaSuccess)
           continue;
@@ -986,9 +989,9 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       auto launch = [&](size_t q, uint64_t first) {
         const Built& b = *bs[q];
         Timed& t = T[q];
-        unsigned long long tb = first;
+        unsigned long long tb = first, stride = b.tasks / t.cnt;
         unsigned tc = (unsigned)t.cnt;
-        void* args[] = {&tb, &tc, &t.d_cnt, &t.d_slots, &t.d_tier};
+        void* args[] = {&tb, &tc, &stride, &t.d_cnt, &t.d_slots, &t.d_tier};
         cudaMemsetAsync(t.d_cnt, 0, 4, st);
         return cudaLaunchKernel((const void*)t.k, dim3(t.grid), dim3(b.sp.threads), args, 0, st);
       };
