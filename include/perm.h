@@ -88,7 +88,11 @@ typedef struct {
   int min_blocks;        /* __launch_bounds__ min blocks per SM (register cap);
                             0 = auto from the planner's register estimate */
   int zero_skip;         /* INT01 zero tracking: 0 = on, -1 = off */
-  int reserved[5];
+  int autotune;          /* 0 = with a device, time the compiled candidates on a
+                            strided sample of their task range and keep a clearly
+                            (>8 %) faster one over the model's pick; -1 = off
+                            (the model's pick: deterministic across processes) */
+  int reserved[4];
 } perm_opts;
 
 /* Result of a computation. */

@@ -66,8 +66,9 @@ def dense_to_crs(A):
 
 def make_opts(mode="auto", device=0, stream=None, chunk_log2=0, block_log2=0, task_chunks=0,
               gr_ratio=0.0, hybrid_c=0, threads_per_block=0, no_device=False, factor_cols=0,
-              min_blocks=0, zero_skip=0) -> perm_opts:
+              min_blocks=0, zero_skip=0, autotune=0) -> perm_opts:
     o = perm_opts()
+    o.autotune = autotune
     o.factor_cols = factor_cols
     o.min_blocks = min_blocks
     o.zero_skip = zero_skip

@@ -24,7 +24,7 @@ class perm_opts(ctypes.Structure):
                 ("gr_ratio", ctypes.c_double), ("hybrid_c", ctypes.c_int),
                 ("threads_per_block", ctypes.c_int), ("no_device", ctypes.c_int),
                 ("factor_cols", ctypes.c_int), ("min_blocks", ctypes.c_int), ("zero_skip", ctypes.c_int),
-                ("reserved", ctypes.c_int * 5)]
+                ("autotune", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
 
 
 class perm_result(ctypes.Structure):

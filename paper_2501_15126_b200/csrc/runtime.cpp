@@ -627,7 +627,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     auto app = [&](const void* d, size_t nb) { pkey.append((const char*)d, nb); };
     const int hdr[] = {n, mode, (int)ord, p->opts.chunk_log2, p->opts.block_log2, p->opts.task_chunks,
                        p->opts.factor_cols, p->opts.min_blocks, p->opts.threads_per_block,
-                       p->opts.hybrid_c, p->opts.zero_skip};
+                       p->opts.hybrid_c, p->opts.zero_skip, p->opts.autotune, p->opts.no_device};
     app(hdr, sizeof hdr);
     app(&gr, sizeof gr);
     app(p->ccs.ptr.data(), p->ccs.ptr.size() * sizeof(int32_t));
@@ -1113,7 +1113,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     size_t pick = 0;
     for (size_t q = 1; q < oks.size(); ++q)
       if (oks[q].score < oks[pick].score) pick = q;
-    if (oks.size() > 1 && !p->opts.no_device && !(getenv("PERM_NO_AUTOTUNE") && atoi(getenv("PERM_NO_AUTOTUNE")))) {
+    if (oks.size() > 1 && !p->opts.no_device && p->opts.autotune >= 0 &&
+        !(getenv("PERM_NO_AUTOTUNE") && atoi(getenv("PERM_NO_AUTOTUNE")))) {
       std::vector<const Built*> bs;
       for (const Ok& o : oks) bs.push_back(&o.b);
       const std::vector<double> t = time_candidates(bs, p->opts.device, p->is_u128 || p->is_c128);

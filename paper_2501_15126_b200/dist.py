@@ -10,6 +10,29 @@ and every rank folds them in rank order with the deterministic fold kernel
 from __future__ import annotations
 
 
+def plan_signature(plan):
+    i = plan.info
+    return (i["K"], i["B"], i["U"], i["M"], i["tasks"], tuple(i["col_perm"]), tuple(i["row_perm"]))
+
+
+def agree_plan(make_plan, world: int, group=None):
+    """Plan on every rank (make_plan(autotune=...) -> Plan).  The planner's
+    autotune may, on a near-tie, pick different kernels on different GPUs; the
+    shards only form one reduction tree if all ranks run the same plan, so on
+    any disagreement every rank re-plans with the deterministic model pick.
+    Returns (plan, autotune setting used)."""
+    plan = make_plan(autotune=0)
+    if world == 1:
+        return plan, 0
+    import torch.distributed as dist
+    sigs = [None] * world
+    dist.all_gather_object(sigs, plan_signature(plan), group=group)
+    if all(s == sigs[0] for s in sigs):
+        return plan, 0
+    plan.close()
+    return make_plan(autotune=-1), -1
+
+
 class ShardedPermanent:
     """Buffers + one-call step for a plan across the ranks of `group`."""
 
@@ -24,10 +47,8 @@ class ShardedPermanent:
             # every rank plans on its own: the shards only form one reduction
             # tree if all ranks chose the same plan (ordering, K, geometry)
             import torch.distributed as dist
-            i = plan.info
-            sig = (i["K"], i["B"], i["U"], i["M"], i["tasks"], tuple(i["col_perm"]), tuple(i["row_perm"]))
             sigs = [None] * world
-            dist.all_gather_object(sigs, sig, group=group)
+            dist.all_gather_object(sigs, plan_signature(plan), group=group)
             if any(s != sigs[0] for s in sigs):
                 raise RuntimeError(f"ranks planned different kernels: {sigs}")
 
