@@ -930,9 +930,19 @@ struct PostStats {
   std::vector<double> region_ops;
   int reg_words = 0;   // 32-bit words of surviving loop-carried registers
   int fused = 0, removed = 0;
+  int smem_bytes = 0;  // per block: loop-carried values moved to shared memory
+  int moved = 0;
 };
 
-PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, size_t nregions, bool fuse) {
+// 4. Shared-memory placement.  A loop-carried value (row, composite cache,
+//    level/suffix product) that the block body never references is only read
+//    and written by the switch cases (once per block at most), yet it would
+//    hold registers through the whole body.  Such values live in shared memory
+//    instead, one 8/16-byte slot per thread (`SM_name`, conflict-free
+//    [slot][thread] layout), which frees the registers the unrolled body
+//    needs (at n=40 29 of 68 loop-carried doubles qualify).
+PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, size_t nregions, bool fuse,
+                    int body_region = -1, int threads = 128) {
   PostStats ps;
   ps.region_ops.assign(nregions, 0.0);
   struct Ln {
@@ -1106,25 +1116,85 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
       l.text = text;
     }
   }
+  // ---- 4. shared-memory placement of values the body never references
+  std::set<int> moved;
+  std::string smem_decl;
+  if (body_region >= 0 && !getenv("PERM_NO_SMEM")) {
+    std::set<int> in_body;
+    for (const Ln& l : L)
+      if (l.alive && l.region == body_region) in_body.insert(l.toks.begin(), l.toks.end());
+    struct Mv { int id, size; std::string ty; };
+    std::vector<Mv> mv;
+    for (const Ln& l : L)
+      if (l.alive && l.kind == 2 && !in_body.count(l.name)) {
+        const std::string& ty = idname[l.toks[0]];
+        mv.push_back({l.name, ty == "int" ? 4 : ((ty == "double" || ty == "i64") ? 8 : 16), ty});
+      }
+    std::stable_sort(mv.begin(), mv.end(), [](const Mv& a, const Mv& b) { return a.size > b.size; });
+    int off = 0;
+    std::ostringstream d;
+    d << "extern __shared__ __align__(16) unsigned char sm_[];  // loop-carried values the block body never touches\n";
+    for (const Mv& m : mv) {
+      d << "#define SM_" << idname[m.id] << " (((" << m.ty << "*)(sm_ + " << off << "))[threadIdx.x])\n";
+      off += m.size * threads;
+      moved.insert(m.id);
+    }
+    if (!mv.empty()) {
+      smem_decl = d.str();
+      ps.smem_bytes = off;
+      ps.moved = (int)mv.size();
+    }
+  }
+  auto rename = [&](Ln& l) {  // moved names -> SM_name (declarations become stores)
+    std::string t;
+    const std::string& s0 = l.text;
+    size_t i = 0;
+    if (l.kind == 2 && moved.count(l.name)) {  // "  TYPE name = expr;" -> "  SM_name = expr;"
+      const size_t p0 = s0.find_first_not_of(' ');
+      const size_t p1 = s0.find(idname[l.name], p0);
+      t = s0.substr(0, p0);
+      i = p1;
+    }
+    while (i < s0.size()) {
+      if (isid0(s0[i]) && (i == 0 || !isid(s0[i - 1]))) {
+        size_t j = i;
+        while (j < s0.size() && isid(s0[j])) ++j;
+        const std::string w = s0.substr(i, j - i);
+        auto it = ids.find(w);
+        if (it != ids.end() && moved.count(it->second)) t += "SM_";
+        t += w;
+        i = j;
+      } else {
+        t += s0[i++];
+      }
+    }
+    l.text = t;
+  };
   std::string out;
-  out.reserve(src.size());
-  for (const Ln& l : L) {
+  out.reserve(src.size() + smem_decl.size());
+  for (Ln& l : L) {
     if (!l.alive) continue;
+    if (!moved.empty()) {
+      bool hit = false;
+      for (int tk : l.toks) hit |= moved.count(tk) > 0;
+      if (hit) rename(l);
+      if (l.text.compare(0, 10, "extern \"C\"") == 0) out += smem_decl;
+    }
     out += l.text;
     out += '\n';
     if (l.kind == 1 && l.region >= 0 && l.region < (int)nregions) {
       auto it = wt.find(idname[l.name]);
       if (it != wt.end()) ps.region_ops[l.region] += it->second;
     }
-    if (l.kind == 2) {
+    if (l.kind == 2 && !moved.count(l.name)) {
       const std::string& ty = idname[l.toks[0]];
       ps.reg_words += ty == "int" ? 1 : ((ty == "double" || ty == "i64") ? 2 : 4);
     }
   }
   src.swap(out);
   if (getenv("PERM_DEBUG_POST"))
-    fprintf(stderr, "[post] lines %zu regions %zu removed %d fused %d regwords %d\n", L.size(), nregions,
-            ps.removed, ps.fused, ps.reg_words);
+    fprintf(stderr, "[post] lines %zu regions %zu removed %d fused %d regwords %d smem %d B (%d values)\n",
+            L.size(), nregions, ps.removed, ps.fused, ps.reg_words, ps.smem_bytes, ps.moved);
   return ps;
 }
 
@@ -1314,7 +1384,9 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
   (void)ops_body;
   (void)ops_switch;
   const bool fuse = !g.i01 && !g.cx && !getenv("PERM_NO_FUSE");
-  const PostStats ps = post_pass(kc.source, g.wt, g.region_weight.size(), fuse);
+  const int body_region = (U > 0 && nblk > 1) ? (int)g.region_weight.size() - 1 : -1;
+  const PostStats ps = post_pass(kc.source, g.wt, g.region_weight.size(), fuse, body_region, S.threads);
+  kc.smem_bytes = ps.smem_bytes;
   double chunk_ops = 1.0;  // + lacc
   for (size_t k = 0; k < ps.region_ops.size(); ++k) chunk_ops += ps.region_ops[k] * g.region_weight[k];
   kc.ops_seed = ps.region_ops.empty() ? 0.0 : ps.region_ops[0];

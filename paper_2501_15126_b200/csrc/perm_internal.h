@@ -73,6 +73,7 @@ struct KernelCode {
   std::string name = "perm_sweep";
   int live_rows = 0, tier_rows = 0, seed_rows = 0, levels = 0;
   int tier_bytes = 0;       // bytes of global tier storage per thread (HYBRID)
+  int smem_bytes = 0;       // dynamic shared memory per block (loop-carried values off the body)
   double ops_seed = 0, ops_block = 0, ops_chunk_total = 0;
   double w_plan = 0;        // arithmetic ops per Gray step
   int est_regs = 0;         // rough register estimate (for __launch_bounds__)

@@ -338,11 +338,15 @@ int load_device_impl(perm_plan_s* p) {
     if (!hit) {
       CUDA_TRY(cudaLibraryLoadData(&le.lib, p->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
       CUDA_TRY(cudaLibraryGetKernel(&le.kern, le.lib, p->code.name.c_str()));
+      if (p->code.smem_bytes > 0)
+        CUDA_TRY(cudaFuncSetAttribute((const void*)le.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      p->code.smem_bytes));
       cudaFuncAttributes fa;
       CUDA_TRY(cudaFuncGetAttributes(&fa, (const void*)le.kern));
       le.regs = fa.numRegs;
       le.local = (int)fa.localSizeBytes;
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&le.bps, (const void*)le.kern, p->spec.threads, 0));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&le.bps, (const void*)le.kern, p->spec.threads,
+                                                             p->code.smem_bytes));
       le.refs = 1;
       std::lock_guard<std::mutex> lk(g_dev_mu);
       auto ins = g_libs.insert({{p->device, p->lib_key}, le});
@@ -367,7 +371,6 @@ int load_device_impl(perm_plan_s* p) {
     if (p->code.tier_bytes > 0) {
       p->tier_alloc_bytes = (size_t)p->code.tier_bytes * (size_t)p->info.grid * (size_t)p->spec.threads;
       CUDA_TRY(pool_alloc(p->device, &p->d_tier, p->tier_alloc_bytes));
-      p->info.smem_bytes = 0;
     }
     lap("buffers");
   }
@@ -393,7 +396,8 @@ int run_range(perm_plan_s* p, uint64_t first, uint64_t count, double* sweep_ms, 
   const int grid = (int)std::min<uint64_t>((uint64_t)p->info.grid,
                                            (count * 32 + p->spec.threads - 1) / p->spec.threads);
   CUDA_TRY(cudaEventRecord(p->ev[0], p->stream));
-  CUDA_TRY(cudaLaunchKernel((const void*)p->kern, dim3(grid), dim3(p->spec.threads), args, 0, p->stream));
+  CUDA_TRY(cudaLaunchKernel((const void*)p->kern, dim3(grid), dim3(p->spec.threads), args,
+                            (size_t)p->code.smem_bytes, p->stream));
   CUDA_TRY(cudaEventRecord(p->ev[1], p->stream));
   CUDA_TRY(libperm_launch_tree_reduce(p->d_slots, count, p->kind(), p->d_partial, p->d_rscratch, p->stream));
   CUDA_TRY(cudaEventRecord(p->ev[2], p->stream));
@@ -970,7 +974,11 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         if (b.tasks == 0 || b.cubin.empty()) continue;
         if (cudaLibraryLoadData(&t.lib, b.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
             cudaLibraryGetKernel(&t.k, t.lib, b.kc.name.c_str()) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void*)t.k, b.sp.threads, 0) != cudaSuccess ||
+            (b.kc.smem_bytes > 0 &&
+             cudaFuncSetAttribute((const void*)t.k, cudaFuncAttributeMaxDynamicSharedMemorySize, b.kc.smem_bytes) !=
+                 cudaSuccess) ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void*)t.k, b.sp.threads, b.kc.smem_bytes) !=
+                cudaSuccess ||
             bps < 1)
           continue;
         const uint64_t grid = (uint64_t)bps * sms, warps = grid * b.sp.threads / 32;
@@ -993,7 +1001,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         unsigned tc = (unsigned)t.cnt;
         void* args[] = {&tb, &tc, &stride, &t.d_cnt, &t.d_slots, &t.d_tier};
         cudaMemsetAsync(t.d_cnt, 0, 4, st);
-        return cudaLaunchKernel((const void*)t.k, dim3(t.grid), dim3(b.sp.threads), args, 0, st);
+        return cudaLaunchKernel((const void*)t.k, dim3(t.grid), dim3(b.sp.threads), args, (size_t)b.kc.smem_bytes,
+                                st);
       };
       auto sample = [&](size_t q) -> double {  // seconds per Gray step of one round
         const Built& b = *bs[q];
@@ -1166,6 +1175,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       I.tier_rows = p->code.tier_rows;
       I.seed_rows = p->code.seed_rows;
       I.levels = p->code.levels;
+      I.smem_bytes = p->code.smem_bytes;
       I.block = p->spec.threads;
     }
     std::lock_guard<std::mutex> lk(g_cache_mu);
