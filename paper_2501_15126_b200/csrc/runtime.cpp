@@ -982,9 +982,12 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
             bps < 1)
           continue;
         const uint64_t grid = (uint64_t)bps * sms, warps = grid * b.sp.threads / 32;
-        // one strided launch: tasks spread over the whole range (every task bit varies)
+        // one strided launch: tasks spread over the whole range (every task bit
+        // varies); about four waves, one wave when tasks are long (> 2^27 Gray steps)
+        const double task_gray = 32.0 * b.sp.M * std::ldexp(1.0, b.sp.B + b.sp.K);
+        const uint64_t waves = task_gray > std::ldexp(1.0, 27) ? 1 : 4;
         t.cnt = 1;
-        while (t.cnt * 2 <= std::min<uint64_t>(b.tasks, 4 * warps)) t.cnt *= 2;
+        while (t.cnt * 2 <= std::min<uint64_t>(b.tasks, waves * warps)) t.cnt *= 2;
         t.S = 1;
         t.grid = (unsigned)std::min<uint64_t>(grid, (t.cnt * 32 + b.sp.threads - 1) / b.sp.threads);
         if (cudaMalloc(&t.d_cnt, 256) != cudaSuccess || cudaMalloc(&t.d_slots, t.cnt * (wide ? 16 : 8)) != cudaSuccess)
@@ -1014,11 +1017,22 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         if (!okl || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) return -1.0;
         return ms * 1e-3 / ((double)t.S * t.cnt * 32.0 * b.sp.M * std::ldexp(1.0, b.sp.B + b.sp.K));
       };
-      for (size_t q = 0; q < bs.size(); ++q)  // warm-up (module load, clock ramp)
-        if (T[q].ok && sample(q) < 0) T[q].ok = false;
+      // warm-up (module load, clock ramp); a candidate whose sample already
+      // takes > 50 ms (large n: long tasks) keeps that single measurement
+      std::vector<char> long_sample(bs.size(), 0);
+      for (size_t q = 0; q < bs.size(); ++q) {
+        if (!T[q].ok) continue;
+        const auto t0 = std::chrono::steady_clock::now();
+        const double v = sample(q);
+        if (v < 0) { T[q].ok = false; continue; }
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > 0.05) {
+          long_sample[q] = 1;
+          out[q] = v;
+        }
+      }
       for (int round = 0; round < 3; ++round)
         for (size_t q = 0; q < bs.size(); ++q) {
-          if (!T[q].ok) continue;
+          if (!T[q].ok || long_sample[q]) continue;
           const double v = sample(q);
           if (v < 0) { T[q].ok = false; out[q] = -1.0; continue; }
           out[q] = out[q] < 0 ? v : std::min(out[q], v);
