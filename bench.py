@@ -325,9 +325,10 @@ def main():
         traffic, traffic_src = None, None
         tpath = os.path.join(ROOT, "profiles", "r1_bench_kernel_ncu.json")
         if os.path.exists(tpath):
-            t = json.load(open(tpath))
             sig = {k: info[k] for k in ("n", "nnz", "K", "B", "U", "M", "tasks", "w_plan")}
-            if t.get("signature") == sig:
+            for t in json.load(open(tpath)).get("entries", []):  # one entry per audited plan
+                if t.get("signature") != sig:
+                    continue
                 traffic, traffic_src = t["dram_bytes_per_launch"], t["source"]
                 if t.get("w_exec"):
                     # nvcc's own CSE across the switch join removes ~3 % of the

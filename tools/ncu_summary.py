@@ -133,7 +133,10 @@ def main():
             out["w_exec"] = dp / gray
             out["w_exec_over_w_plan"] = out["w_exec"] / info["w_plan"]
             shutil.copy(a.dpaudit, os.path.join(prof, f"{a.round}_dpaudit_bench.csv"))
-        json.dump(out, open(os.path.join(prof, f"{a.round}_bench_kernel_ncu.json"), "w"), indent=1)
+        path = os.path.join(prof, f"{a.round}_bench_kernel_ncu.json")
+        entries = json.load(open(path)).get("entries", []) if os.path.exists(path) else []
+        entries = [e for e in entries if e.get("signature") != sig] + [out]  # one entry per audited plan
+        json.dump({"entries": entries}, open(path, "w"), indent=1)
         print("\n", json.dumps(out))
 
 
