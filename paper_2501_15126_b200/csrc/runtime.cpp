@@ -1132,7 +1132,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     // model choice; then, with a device, measured choice (autotune): each
     // compiled candidate sweeps a few spread samples of its task range, and
     // replaces the model's pick only when it is clearly faster per Gray step
-    // (> 8 %), so near-ties stay deterministic across ranks
+    // (> 4 %), so near-ties stay deterministic across ranks
     size_t pick = 0;
     for (size_t q = 1; q < oks.size(); ++q)
       if (oks[q].score < oks[pick].score) pick = q;
@@ -1145,7 +1145,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         size_t best = pick;
         for (size_t q = 0; q < oks.size(); ++q)
           if (t[q] > 0 && t[q] < t[best]) best = q;
-        if (best != pick && t[best] < 0.92 * t[pick]) pick = best;
+        if (best != pick && t[best] < 0.96 * t[pick]) pick = best;
       }
       if (dbg_plan)
         for (size_t q = 0; q < oks.size(); ++q)
