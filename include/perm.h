@@ -90,7 +90,7 @@ typedef struct {
   int zero_skip;         /* INT01 zero tracking: 0 = on, -1 = off */
   int autotune;          /* 0 = with a device, time the compiled candidates on a
                             strided sample of their task range and keep a clearly
-                            (>8 %) faster one over the model's pick; -1 = off
+                            (>4 %) faster one over the model's pick; -1 = off
                             (the model's pick: deterministic across processes) */
   int reserved[4];
 } perm_opts;
