@@ -687,10 +687,16 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     std::vector<std::vector<int>> row_cols(n);
     for (int j = 0; j < n; ++j)
       for (int q = p->ccs.ptr[j]; q < p->ccs.ptr[j + 1]; ++q) row_cols[p->ccs.idx[q]].push_back(j);
-    auto zero_aware = [&](const std::vector<int>& colp, int K, int B, double& pskip) {
+    // Rows placed only on block-level bits [U, B) are lane-uniform too and
+    // constant within a block: when one is 0, S_U == 0 on every lane and the
+    // existing block-level skip drops the block.  The placement fills the top
+    // (chunk-skip) positions first, then [U, B).
+    auto zero_aware = [&](const std::vector<int>& colp, int K, int B, int U, double& pskip) {
       pskip = 0;
-      const int top = (n - 1 - K) - B - 5;
+      const int nb = n - 1 - K;
+      const int top = std::max(0, nb - B - 5), mid = std::max(0, B - std::max(U, 0));
       if (top < 1) return colp;
+      const int cap = std::min(top + mid, 31);
       const int last = colp[n - 1];
       std::set<int> elim(colp.begin(), colp.begin() + K);
       struct R { double pz; int r; };
@@ -709,11 +715,14 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       }
       std::stable_sort(rows.begin(), rows.end(), [](const R& a, const R& b) { return a.pz > b.pz; });
       std::set<int> chosen_cols;
+      std::vector<int> chosen_order;  // priority: columns of the most zero-prone rows first
       double keep = 1.0;
       for (const R& x : rows) {
         std::set<int> u = chosen_cols;
         for (int c : row_cols[x.r]) if (c != last) u.insert(c);
-        if ((int)u.size() > std::min(top, 31)) continue;
+        if ((int)u.size() > cap) continue;
+        for (int c : row_cols[x.r])
+          if (c != last && !chosen_cols.count(c)) chosen_order.push_back(c);
         chosen_cols.swap(u);
         keep *= 1.0 - x.pz;
       }
@@ -758,19 +767,30 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         }
         pskip = tot ? (double)hit / (double)tot : 0.0;
       }
-      std::vector<int> out(colp.begin(), colp.begin() + K), hi;
-      for (int q = K; q < n - 1; ++q) (chosen_cols.count(colp[q]) ? hi : out).push_back(colp[q]);
-      out.insert(out.end(), hi.begin(), hi.end());
+      // swept slots: chosen columns on the top positions, the rest of them on
+      // [U, B) (highest first); the other columns keep their relative order
+      std::vector<int> slot(nb, -1);
+      const int ntop = std::min((int)chosen_order.size(), top);
+      for (int q = 0; q < ntop; ++q) slot[nb - 1 - q] = chosen_order[q];
+      for (int q = ntop; q < (int)chosen_order.size(); ++q) slot[B - 1 - (q - ntop)] = chosen_order[q];
+      int w = 0;
+      for (int q = K; q < n - 1; ++q) {
+        if (chosen_cols.count(colp[q])) continue;
+        while (slot[w] >= 0) ++w;
+        slot[w] = colp[q];
+      }
+      std::vector<int> out(colp.begin(), colp.begin() + K);
+      out.insert(out.end(), slot.begin(), slot.end());
       out.push_back(last);
       return out;
     };
     auto colp_of = [&](const std::vector<int>& cp, const std::vector<int>& picks, int K, int var, int B = 0,
-                       double* pskip = nullptr) {
+                       double* pskip = nullptr, int U = -1) {
       std::vector<int> c = factored_columns(cp, picks, K);
-      if (var == 2) {  // zero-aware placement on top of the cost-sorted order (INT01)
+      if (var >= 2) {  // zero-aware placement on the cost-sorted order (INT01); 3: also on [U, B)
         c = costsort_swept(p->ccs, c, K);
         double ps = 0;
-        c = zero_aware(c, K, B, ps);
+        c = zero_aware(c, K, B, var == 3 ? U : B, ps);
         if (pskip) *pskip = ps;
         return c;
       }
@@ -882,8 +902,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       const int kmax = (int)picks.size();
       const int kmin = p->opts.factor_cols > 0 ? kmax : (ev == 0 ? 0 : std::max(0, kmax - 2));
       for (int K = kmin; K <= kmax; ++K)
-        for (int var = 0; var < nvar + (mode == PERM_MODE_INT01 && p->opts.zero_skip >= 0 ? 1 : 0); ++var) {
-          const int vv = var < nvar ? var : 2;
+        for (int var = 0; var < nvar + (mode == PERM_MODE_INT01 && p->opts.zero_skip >= 0 ? 2 : 0); ++var) {
+          const int vv = var < nvar ? var : 2 + (var - nvar);
           Csx o = permute_ccs(p->ccs, rp, colp_of(cp, picks, K, vv));
           std::vector<double> xo = make_x0(o);
           std::set<int> seenB;
@@ -893,8 +913,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
             set_hybrid(sp, o);
             if (!seenB.insert(sp.B).second) continue;  // cap not binding: duplicate
             double pskip = 0;
-            if (vv == 2) {  // the placement depends on B
-              o = permute_ccs(p->ccs, rp, colp_of(cp, picks, K, 2, sp.B, &pskip));
+            if (vv >= 2) {  // the placement depends on B (and U)
+              o = permute_ccs(p->ccs, rp, colp_of(cp, picks, K, vv, sp.B, &pskip, sp.U));
               xo = make_x0(o);
               if (pskip <= 0) continue;
             }
@@ -916,9 +936,20 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       for (const Cand& c : cands)
         fprintf(stderr, "[plan] cand score %.5f w %.5f base %d K %d var %d bcap %d est %d cc %d pskip %.3f\n", c.score, c.w,
                 c.base, c.K, c.var, c.bcap, c.est, (int)c.cc, c.pskip);
-    {
-      const size_t ncomp = getenv("PERM_PLAN_COMPILES") ? (size_t)atoi(getenv("PERM_PLAN_COMPILES")) : 4;
-      if (cands.size() > ncomp) cands.resize(ncomp);
+    {  // the top ncomp by model score, plus the best of every swept-order
+       // variant not among them (the model's skip / occupancy estimates are
+       // rough; autotune compares the variants on the device)
+      const size_t ncomp = getenv("PERM_PLAN_COMPILES") ? (size_t)atoi(getenv("PERM_PLAN_COMPILES")) : 3;
+      std::vector<Cand> keep;
+      std::set<int> vars;
+      for (size_t q = 0; q < cands.size(); ++q)
+        if (q < ncomp) {
+          keep.push_back(cands[q]);
+          vars.insert(cands[q].var);
+        }
+      for (size_t q = ncomp; q < cands.size() && keep.size() < ncomp + 3; ++q)
+        if (vars.insert(cands[q].var).second) keep.push_back(cands[q]);
+      cands.swap(keep);
     }
     if (p->singular || n == 1) cands.resize(std::min<size_t>(cands.size(), 1));
     // compile the top candidates (NVRTC, spill gate with escalation) and keep
@@ -1055,7 +1086,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       std::vector<int> cp;
       order_with(c.base, b.rp, cp);
       b.tasks = geometry(c.K, b.sp, c.bcap);
-      b.colp = colp_of(cp, elim_of_base[c.base * 8 + c.ev], c.K, c.var, b.sp.B);
+      b.colp = colp_of(cp, elim_of_base[c.base * 8 + c.ev], c.K, c.var, b.sp.B, nullptr, b.sp.U);
       b.o = permute_ccs(p->ccs, b.rp, b.colp);
       b.xo = make_x0(b.o);
       b.sp.cc = c.cc;
