@@ -292,3 +292,17 @@ def test_int01_zero_aware_placement_is_chosen_for_binary_er():
     assert i["swept_order"] in (2, 3) and i["seed_rows"] > 0
     assert "__all_sync(0xffffffffu, F == 0)" in P.source
     assert sorted(i["col_perm"]) == list(range(40))
+
+
+def test_maximum_size_n64_plans_full_gray_range():
+    """n = 64 (the u64 Gray-index limit): the plan covers exactly 2^63 Gray
+    steps with a power-of-two task grid and no local memory."""
+    A = synth.givens_brickwork(64, 4, 1)
+    P = pb.Plan.from_dense(A, mode="reg", no_device=True)
+    i = P.info
+    assert i["local_bytes"] == 0 and i["w_plan"] > 0
+    assert i["tasks"] & (i["tasks"] - 1) == 0
+    steps = i["tasks"] * 32 * i["M"] * (1 << i["B"]) * (1 << i["K"])
+    assert steps == 2 ** 63
+    r = P.shard_range(0, 1)
+    assert r[-1] == 2 ** 63
