@@ -1,3 +1,5 @@
+"""Plan + time a few bench-like workloads on cuda:0 (PERM_DEBUG_PLAN=1 shows the
+planner candidates and autotune measurements)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth, paper_2501_15126_b200 as pb
