@@ -949,6 +949,26 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         }
       for (size_t q = ncomp; q < cands.size() && keep.size() < ncomp + 3; ++q)
         if (vars.insert(cands[q].var).second) keep.push_back(cands[q]);
+      // zero-aware placements (INT01): the skip model is the roughest, so the
+      // two best of each such variant (B changes the placed columns) get measured
+      for (int zv = 2; zv <= 3; ++zv) {
+        int have_v = 0;
+        for (const Cand& c : keep) have_v += c.var == zv;
+        for (size_t q = 0; q < cands.size() && have_v < 2 && keep.size() < ncomp + 5; ++q) {
+          const Cand& c = cands[q];
+          if (c.var != zv) continue;
+          bool dup = false;
+          for (const Cand& k2 : keep)
+            dup |= k2.var == c.var && k2.K == c.K && k2.bcap == c.bcap && k2.base == c.base && k2.ev == c.ev &&
+                   k2.cc == c.cc;
+          if (dup) continue;
+          bool same_geo = false;  // prefer a different B (a different placement) for the second
+          for (const Cand& k2 : keep) same_geo |= k2.var == zv && k2.bcap == c.bcap;
+          if (same_geo && have_v > 0) continue;
+          keep.push_back(c);
+          ++have_v;
+        }
+      }
       cands.swap(keep);
     }
     if (p->singular || n == 1) cands.resize(std::min<size_t>(cands.size(), 1));
