@@ -1051,7 +1051,10 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       auto launch = [&](size_t q, uint64_t first) {
         const Built& b = *bs[q];
         Timed& t = T[q];
-        unsigned long long tb = first, stride = b.tasks / t.cnt;
+        // odd stride: the sampled task indices vary in their low bits too (a
+        // power-of-two stride pins them, biasing the zero-skip rate); indices
+        // past the range wrap in the seed (bits >= n-1-K are ignored): valid states
+        unsigned long long tb = first, stride = (b.tasks / t.cnt) | 1ull;
         unsigned tc = (unsigned)t.cnt;
         void* args[] = {&tb, &tc, &stride, &t.d_cnt, &t.d_slots, &t.d_tier};
         cudaMemsetAsync(t.d_cnt, 0, 4, st);
