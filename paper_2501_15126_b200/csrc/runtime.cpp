@@ -1005,7 +1005,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       unsigned grid = 0;
       bool ok = false;
     };
-    auto time_candidates = [&](const std::vector<const Built*>& bs, int device, bool wide) {
+    auto time_candidates = [&](const std::vector<const Built*>& bs, const std::vector<double>& pskips, int device,
+                               bool wide) {
       std::vector<double> out(bs.size(), -1.0);
       std::vector<Timed> T(bs.size());
       cudaStream_t st = nullptr;
@@ -1036,7 +1037,10 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         // one strided launch: tasks spread over the whole range (every task bit
         // varies); about four waves, one wave when tasks are long (> 2^27 Gray steps)
         const double task_gray = 32.0 * b.sp.M * std::ldexp(1.0, b.sp.B + b.sp.K);
-        const uint64_t waves = task_gray > std::ldexp(1.0, 27) ? 1 : 4;
+        // zero-skip plans: most tasks are nearly free and the sample's makespan
+        // is set by the few full ones, so it needs ~4 waves of *unskipped* tasks
+        const double keep = std::max(0.02, 1.0 - pskips[q]);
+        const uint64_t waves = task_gray > std::ldexp(1.0, 27) ? 1 : (uint64_t)std::ceil(4.0 / keep);
         t.cnt = 1;
         while (t.cnt * 2 <= std::min<uint64_t>(b.tasks, waves * warps)) t.cnt *= 2;
         t.S = 1;
@@ -1193,8 +1197,12 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     if (oks.size() > 1 && !p->opts.no_device && p->opts.autotune >= 0 &&
         !(getenv("PERM_NO_AUTOTUNE") && atoi(getenv("PERM_NO_AUTOTUNE")))) {
       std::vector<const Built*> bs;
-      for (const Ok& o : oks) bs.push_back(&o.b);
-      const std::vector<double> t = time_candidates(bs, p->opts.device, p->is_u128 || p->is_c128);
+      std::vector<double> pskips;
+      for (const Ok& o : oks) {
+        bs.push_back(&o.b);
+        pskips.push_back(cands[o.ci].pskip);
+      }
+      const std::vector<double> t = time_candidates(bs, pskips, p->opts.device, p->is_u128 || p->is_c128);
       if (t[pick] > 0) {
         size_t best = pick;
         for (size_t q = 0; q < oks.size(); ++q)
