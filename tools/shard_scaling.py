@@ -14,7 +14,7 @@ import paper_2501_15126_b200 as pb  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=40)
+    ap.add_argument("--dim", dest="n", type=int, default=40)
     ap.add_argument("--p", type=float, default=0.2)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--worlds", default="2,4,8")
