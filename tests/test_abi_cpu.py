@@ -306,3 +306,17 @@ def test_maximum_size_n64_plans_full_gray_range():
     assert steps == 2 ** 63
     r = P.shard_range(0, 1)
     assert r[-1] == 2 ** 63
+
+
+def test_smem_placement_of_values_the_body_never_touches():
+    """DESIGN 3.13(d): loop-carried values absent from the block body live in
+    per-thread shared-memory slots; none of them appears in the body."""
+    A = synth.erdos_renyi(40, 0.2, 1)
+    P = pb.Plan.from_dense(A, mode="reg", no_device=True, autotune=-1)
+    src, i = P.source, P.info
+    names = re.findall(r"#define SM_(\w+) ", src)
+    assert names and i["smem_bytes"] >= 128 * 8 * len(names) // 2
+    body = src[src.index("const double sU"):src.index("lacc += cacc")]
+    for nm_ in names:
+        assert not re.search(rf"\b{nm_}\b", body) and f"SM_{nm_}" not in body
+    assert "extern __shared__" in src
