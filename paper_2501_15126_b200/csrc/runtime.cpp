@@ -805,7 +805,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     // complex values take 4 registers: halve the composite size bound
     const int elim_maxsize = getenv("PERM_ELIM_MAXSIZE") ? atoi(getenv("PERM_ELIM_MAXSIZE"))
                                                          : (mode == PERM_MODE_COMPLEX_INTERNAL ? 40 : 96);
-    const int elim_maxsize_big = 160;
+    const int elim_maxsize_big = 160, elim_maxsize_huge = 256;
     // beam width of the elimination searches (FP64: 4, INT01 / complex: greedy)
     const int elim_beam = std::max(1, getenv("PERM_ELIM_BEAM") ? atoi(getenv("PERM_ELIM_BEAM"))
                                       : (mode == PERM_MODE_COMPLEX_INTERNAL ? 1 : 4));
@@ -823,7 +823,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         Csx o = permute_ccs(p->ccs, rp, c);
         KernelSpec sp;
         geometry(k, sp, 8);
-        const int sc = ev % 3;  // scoring; (ev / 3) % 2: greedy (0) or beam (1); ev / 6: large composites
+        const int sc = ev % 3;  // scoring; (ev / 3) % 2: greedy (0) or beam (1); ev / 6: composite bound tier
         sp.U = std::min(sp.U, sc == 2 ? 3 : 4);
         sp.cc = cc_allowed;
         set_hybrid(sp, o);
@@ -858,7 +858,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
             if (!seen.insert(key).second) continue;
             // bound the composite factors' evaluation size (code size, registers)
             if (elim_eval_size(p->ccs, factored_columns(cp, s2, k + 1), k + 1) >
-                (ev >= 6 ? elim_maxsize_big : elim_maxsize))
+                (ev >= 12 ? elim_maxsize_huge : (ev >= 6 ? elim_maxsize_big : elim_maxsize)))
               continue;
             jobs.emplace_back(s2, std::async(std::launch::async, evalW, s2));
           }
@@ -875,19 +875,19 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       }
       return best.second;
     };
-    std::map<int, std::vector<int>> elim_of_base;  // key: base * 16 + ev
+    std::map<int, std::vector<int>> elim_of_base;  // key: base * 32 + ev
     const bool fp64 = mode == PERM_MODE_REG || mode == PERM_MODE_HYBRID;
     // ev = scoring (ev % 3) x search (ev / 3: greedy, beam of width elim_beam)
-    // FP64 also repeats every search with a larger composite bound (160 leaf
-    // evaluations): larger composites win on some matrices and lose on others
+    // FP64 also repeats every search with larger composite bounds (160 and 256
+    // leaf evaluations): larger composites win on some matrices and lose on others
     const int nev = getenv("PERM_ELIM_VARIANTS") ? std::max(1, atoi(getenv("PERM_ELIM_VARIANTS")))
-                                                 : (elim_beam > 1 ? (fp64 && !getenv("PERM_ELIM_MAXSIZE") ? 12 : 6) : 3);
+                                                 : (elim_beam > 1 ? (fp64 && !getenv("PERM_ELIM_MAXSIZE") ? 18 : 6) : 3);
     {
       std::vector<std::pair<int, std::future<std::vector<int>>>> runs;  // greedy runs, concurrently
       for (int base : bases)
         for (int ev = 0; ev < nev; ++ev) {
           if (ev % 3 == 1 && !fp64) continue;
-          runs.emplace_back(base * 16 + ev, std::async(std::launch::async, [&, base, ev] {
+          runs.emplace_back(base * 32 + ev, std::async(std::launch::async, [&, base, ev] {
                               std::vector<int> rp, cp;
                               order_with(base, rp, cp);
                               return greedy_elim(rp, cp, ev);
@@ -896,11 +896,11 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       for (auto& r : runs) elim_of_base[r.first] = r.second.get();
     }
     for (auto& be : elim_of_base) {
-      const int base = be.first / 16, ev = be.first % 16;
+      const int base = be.first / 32, ev = be.first % 32;
       const std::vector<int>& picks = be.second;
       bool dup = false;  // the same sequence found under another scoring
       for (auto& o2 : elim_of_base)
-        if (o2.first < be.first && o2.first / 16 == base && o2.second == picks) dup = true;
+        if (o2.first < be.first && o2.first / 32 == base && o2.second == picks) dup = true;
       if (dup) continue;
       std::vector<int> rp, cp;
       order_with(base, rp, cp);
@@ -1118,7 +1118,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       std::vector<int> cp;
       order_with(c.base, b.rp, cp);
       b.tasks = geometry(c.K, b.sp, c.bcap);
-      b.colp = colp_of(cp, elim_of_base[c.base * 16 + c.ev], c.K, c.var, b.sp.B, nullptr, b.sp.U);
+      b.colp = colp_of(cp, elim_of_base[c.base * 32 + c.ev], c.K, c.var, b.sp.B, nullptr, b.sp.U);
       b.o = permute_ccs(p->ccs, b.rp, b.colp);
       b.xo = make_x0(b.o);
       b.sp.cc = c.cc;
