@@ -120,7 +120,9 @@ typedef struct {
   int K;                  /* factored leading columns: pairwise row-disjoint ordered
                              columns 0..K-1 summed in closed form; the sweep runs
                              over h-space = states of columns K..n-2 (2^(n-1-K)) */
-  int swept_order;        /* 0: swept columns in base order; 1: sorted by flip cost */
+  int swept_order;        /* 0: swept columns in base order; 1: sorted by flip cost;
+                             2 / 3 (INT01): zero-aware placement of zero-prone rows
+                             on lane-uniform bits >= B+5 (3: also on [U, B)) */
   uint64_t tasks;         /* warp-tasks over the whole h-range (power of two);
                              task t covers h in [t*L, (t+1)*L), L = 32*M*2^B, i.e.
                              Gray steps g in [t*L*2^K, (t+1)*L*2^K); its partial
@@ -134,7 +136,9 @@ typedef struct {
                              generated code, incl. amortised seeding */
   double w_alg1;          /* FP64 ops per step of Alg. 1 as written */
   int block, grid, blocks_per_sm, sms;
-  int regs_per_thread, local_bytes, smem_bytes;
+  int regs_per_thread, local_bytes;
+  int smem_bytes;         /* dynamic shared memory per block: loop-carried values the
+                             unrolled block body never references (per-thread slots) */
   double plan_ms, codegen_ms, nvrtc_ms;
   int cubin_cached;       /* 1 if the cubin came from the in-process cache */
   int plan_cached;        /* 1 if ordering/codegen/NVRTC came from the in-process
