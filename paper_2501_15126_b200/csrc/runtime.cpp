@@ -954,6 +954,18 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         }
       for (size_t q = ncomp; q < cands.size() && keep.size() < ncomp + 3; ++q)
         if (vars.insert(cands[q].var).second) keep.push_back(cands[q]);
+      // one fewer eliminated column than the favourite: bigger composites need
+      // more registers than the estimate says, and when the favourite has to
+      // drop to a small U, K-1 at a larger U can be faster (autotune decides)
+      if (!keep.empty() && keep[0].K > 0) {
+        bool have_km1 = false;
+        for (const Cand& k2 : keep) have_km1 |= k2.K == keep[0].K - 1;
+        for (size_t q = ncomp; q < cands.size() && !have_km1; ++q)
+          if (cands[q].K == keep[0].K - 1) {
+            keep.push_back(cands[q]);
+            have_km1 = true;
+          }
+      }
       // zero-aware placements (INT01): the skip model is the roughest, so the
       // two best of each such variant (B changes the placed columns) get measured
       for (int zv = 2; zv <= 3; ++zv) {
