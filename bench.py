@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo + --same-device: test the multi-rank path with ranks sharing one GPU")
     ap.add_argument("--same-device", action="store_true")
+    ap.add_argument("--autotune", action="store_true",
+                    help="let the planner time its compiled candidates on the device (default: the "
+                         "deterministic model pick, so every run and rank times the same kernel)")
     return ap.parse_args()
 
 
@@ -242,8 +245,12 @@ def main():
               block_log2=args.block_log2, task_chunks=args.task_chunks)
     ptr, idx, val = pb.dense_to_ccs(A)
     from paper_2501_15126_b200.dist import ShardedPermanent, agree_plan
-    plan, kw["autotune"] = agree_plan(lambda **a: pb.Plan(n, pb.PERM_CCS, ptr, idx, val, args.ordering, **kw, **a),
-                                      world)
+    if args.autotune:
+        plan, kw["autotune"] = agree_plan(
+            lambda **a: pb.Plan(n, pb.PERM_CCS, ptr, idx, val, args.ordering, **kw, **a), world)
+    else:
+        kw["autotune"] = -1
+        plan = pb.Plan(n, pb.PERM_CCS, ptr, idx, val, args.ordering, **kw)
     info = plan.info
     sp = ShardedPermanent(plan, rank, world, dev)
     out = sp.out
