@@ -355,6 +355,7 @@ def main():
                        "B": info["B"], "U": info["U"], "M": info["M"], "tasks": info["tasks"],
                        "regs": info["regs_per_thread"], "grid": info["grid"], "block": info["block"],
                        "w_plan_fp64_ops_per_step": info["w_plan"], "w_alg1_ops_per_step": info["w_alg1"],
+                       "K": info["K"], "plan_choice": "autotune" if kw["autotune"] == 0 else "model",
                        "vs_baseline_ref": "paper CodeGen-Hybrid A100 n=40 p=0.2: 3.94 s (P:627), context only"},
             "result": result,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
