@@ -161,6 +161,25 @@ def cpu_baseline(A, target_s: float):
                       f"= 2^{length.bit_length() - 1} of the 2^{n - 1} steps, {dt:.2f} s"}
 
 
+def env_info(dev: int) -> dict:
+    """GPU model, driver, CUDA and NCCL versions (SURVEY 8(d) timing protocol)."""
+    import torch
+    out = {"gpu": torch.cuda.get_device_name(dev), "cuda_runtime": torch.version.cuda,
+           "sms": torch.cuda.get_device_properties(dev).multi_processor_count}
+    try:
+        out["nccl"] = ".".join(str(x) for x in torch.cuda.nccl.version())
+    except Exception:
+        pass
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        d = nv.nvmlSystemGetDriverVersion()
+        out["driver"] = d.decode() if isinstance(d, bytes) else d
+    except Exception:
+        pass
+    return out
+
+
 def launches_per_step(slots: int) -> int:
     """Our kernels per step: the sweep, the tree-reduction passes over the
     warp-task slots (512 per block per pass), the fold."""
@@ -366,6 +385,7 @@ def main():
                                      "DADD/DMUL/DFMA lane-op (datasheet FP64 / 2)",
                          "alg1_equiv_frac": info["w_alg1"] * products / (sw / 1000.0) / 1e12 / peak},
             "clocks": clocks,
+            "env": env_info(local),
             "e2e": {"value": e2e_value, "unit": "Gray-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 8,
                     "what": "perm_plan from the host CCS arrays every step (validation, structural rank, planner-cache "
