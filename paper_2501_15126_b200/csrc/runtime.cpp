@@ -805,7 +805,9 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     // complex values take 4 registers: halve the composite size bound
     const int elim_maxsize = getenv("PERM_ELIM_MAXSIZE") ? atoi(getenv("PERM_ELIM_MAXSIZE"))
                                                          : (mode == PERM_MODE_COMPLEX_INTERNAL ? 40 : 96);
-    const int elim_maxsize_big = 160, elim_maxsize_huge = 256;
+    // larger composite-bound tiers (ev / 6 = 1, 2): FP64 160 / 256, complex 64 / 96
+    const bool cplx_mode = mode == PERM_MODE_COMPLEX_INTERNAL;
+    const int elim_maxsize_big = cplx_mode ? 64 : 160, elim_maxsize_huge = cplx_mode ? 96 : 256;
     // beam width of the elimination searches (FP64: 4, INT01 / complex: greedy)
     const int elim_beam = std::max(1, getenv("PERM_ELIM_BEAM") ? atoi(getenv("PERM_ELIM_BEAM"))
                                       : (mode == PERM_MODE_COMPLEX_INTERNAL ? 1 : 4));
@@ -880,13 +882,14 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     // ev = scoring (ev % 3) x search (ev / 3: greedy, beam of width elim_beam)
     // FP64 also repeats every search with larger composite bounds (160 and 256
     // leaf evaluations): larger composites win on some matrices and lose on others
-    const int nev = getenv("PERM_ELIM_VARIANTS") ? std::max(1, atoi(getenv("PERM_ELIM_VARIANTS")))
-                                                 : (elim_beam > 1 ? (fp64 && !getenv("PERM_ELIM_MAXSIZE") ? 18 : 6) : 3);
+    const bool tiers = (fp64 || cplx_mode) && !getenv("PERM_ELIM_MAXSIZE");
+    const int nev = getenv("PERM_ELIM_VARIANTS") ? std::max(1, atoi(getenv("PERM_ELIM_VARIANTS"))) : (tiers ? 18 : 6);
     {
       std::vector<std::pair<int, std::future<std::vector<int>>>> runs;  // greedy runs, concurrently
       for (int base : bases)
         for (int ev = 0; ev < nev; ++ev) {
           if (ev % 3 == 1 && !fp64) continue;
+          if ((ev / 3) % 2 == 1 && elim_beam == 1) continue;  // greedy only: the beam run would repeat it
           runs.emplace_back(base * 32 + ev, std::async(std::launch::async, [&, base, ev] {
                               std::vector<int> rp, cp;
                               order_with(base, rp, cp);
