@@ -898,6 +898,9 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         }
       for (auto& r : runs) elim_of_base[r.first] = r.second.get();
     }
+    // candidates per distinct sequence, generated concurrently and merged in
+    // sequence order (deterministic)
+    std::vector<std::future<std::vector<Cand>>> cjobs;
     for (auto& be : elim_of_base) {
       const int base = be.first / 32, ev = be.first % 32;
       const std::vector<int>& picks = be.second;
@@ -905,6 +908,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       for (auto& o2 : elim_of_base)
         if (o2.first < be.first && o2.first / 32 == base && o2.second == picks) dup = true;
       if (dup) continue;
+      cjobs.push_back(std::async(std::launch::async, [&, base, ev]() {  // picks: map element, stable
+      std::vector<Cand> cands;
       std::vector<int> rp, cp;
       order_with(base, rp, cp);
       const int kmax = (int)picks.size();
@@ -937,6 +942,12 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
             }
           }
         }
+      return cands;
+      }));
+    }
+    for (auto& j : cjobs) {
+      std::vector<Cand> part = j.get();
+      cands.insert(cands.end(), part.begin(), part.end());
     }
     std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.score < b.score; });
     const bool dbg_plan = getenv("PERM_DEBUG_PLAN") != nullptr;
