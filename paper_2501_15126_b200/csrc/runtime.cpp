@@ -805,7 +805,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     // complex values take 4 registers: halve the composite size bound
     const int elim_maxsize = getenv("PERM_ELIM_MAXSIZE") ? atoi(getenv("PERM_ELIM_MAXSIZE"))
                                                          : (mode == PERM_MODE_COMPLEX_INTERNAL ? 40 : 96);
-    // larger composite-bound tiers (ev / 6 = 1, 2): FP64 160 / 256, complex 64 / 96
+    // larger composite-bound tiers (ev / 6 = 1, 2): real (FP64, INT01) 160 / 256, complex 64 / 96
     const bool cplx_mode = mode == PERM_MODE_COMPLEX_INTERNAL;
     const int elim_maxsize_big = cplx_mode ? 64 : 160, elim_maxsize_huge = cplx_mode ? 96 : 256;
     // beam width of the elimination searches (FP64: 4, INT01 / complex: greedy)
@@ -882,7 +882,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     // ev = scoring (ev % 3) x search (ev / 3: greedy, beam of width elim_beam)
     // FP64 also repeats every search with larger composite bounds (160 and 256
     // leaf evaluations): larger composites win on some matrices and lose on others
-    const bool tiers = (fp64 || cplx_mode) && !getenv("PERM_ELIM_MAXSIZE");
+    const bool tiers = !getenv("PERM_ELIM_MAXSIZE");  // every mode: FP64, INT01, complex
     const int nev = getenv("PERM_ELIM_VARIANTS") ? std::max(1, atoi(getenv("PERM_ELIM_VARIANTS"))) : (tiers ? 18 : 6);
     {
       std::vector<std::pair<int, std::future<std::vector<int>>>> runs;  // greedy runs, concurrently
