@@ -42,6 +42,12 @@
 //    (Sec. II-A), which bounds incremental x drift to 2^B steps.
 //  * Lane partials: pairwise inside a block, sequential over blocks and chunks,
 //    then a fixed xor-shuffle tree per warp-task (deterministic slot).
+//  * A whole-kernel post-pass (post_pass) removes dead code, contracts
+//    single-use products into explicit FMAs, recounts the executed DP
+//    instructions per region and moves loop-carried values the block body
+//    never references into per-thread shared-memory slots.
+//  * INT01 values are typed int / i64 / wrapping u128 by magnitude bounds; the
+//    chunk loop skips a chunk when its frozen product is 0 on all 32 lanes.
 #include <algorithm>
 #include <cctype>
 #include <cmath>
