@@ -14,8 +14,13 @@ Functions (each cites its passage; P:n = /root/reference/PAPER.md line n):
   nw2_range_exact   Alg. 1 in exact doubled integers (integer inputs)
   perm_band         band DP (exact textbook evaluation of Eq. 1 for banded A)
   structural_rank   maximum bipartite matching
-Parity status of every function is pinned in tests/test_oracle.py; none is
-"parity unpinned".
+  nw_range_complex, perm_naive_complex, perm_band_complex, perm_nw_complex
+                    the same over C (complex long double)
+oracle/planner.py restates Sec. IV (Theorem 1, SCBS, Lemma 1/2), Alg. 2, Alg. 3,
+the degree sort and Alg. 4, and nothing else.
+Every function is pinned against something other than itself in
+tests/test_oracle.py / tests/test_planner_oracle.py (closed forms, brute force,
+printed examples, invariants); none is "parity unpinned".
 """
 from __future__ import annotations
 

@@ -141,51 +141,6 @@ def permanent_ordering(n: int, cptrs, rids, rptrs, cids):
     return rowPerm, colPerm
 
 
-def factored_order(n: int, cptrs, rids, base_colp, K: int):
-    """Column order with K closed-form summed columns in front (DESIGN.md
-    "Factored columns", a B200-design extension of Sec. V's ordering): walk
-    base_colp[0..n-2] and take a column if its rows are disjoint from the rows
-    of the columns already taken, until K are taken; they go first in pick
-    order, the rest keep base order (the base's last column stays last)."""
-    picks, used = [], set()
-    for c in base_colp[: n - 1]:
-        if len(picks) == K:
-            break
-        rows = set(rids[cptrs[c]:cptrs[c + 1]])
-        if rows and not rows & used:
-            picks.append(c)
-            used |= rows
-    if len(picks) != K:
-        raise ValueError("fewer than K row-disjoint columns")
-    return picks + [c for c in base_colp if c not in picks]
-
-
-def costsort_swept(n: int, cptrs, rids, colp, K: int):
-    """Swept columns (positions K..n-2) stably sorted by the flip cost
-    nnz(c) + sum over touched factored groups g of dcost(|g|), dcost = 0, 2,
-    3|g|-1 for |g| = 1, 2, >= 3 (restates the product heuristic)."""
-    grp = {}
-    size = []
-    for k in range(K):
-        c = colp[k]
-        rows = rids[cptrs[c]:cptrs[c + 1]]
-        for r in rows:
-            grp[r] = k
-        size.append(len(rows))
-
-    def dcost(s):
-        return 0 if s <= 1 else (2 if s == 2 else 3 * s - 1)
-
-    def cost(c):
-        rows = rids[cptrs[c]:cptrs[c + 1]]
-        gs = {grp[r] for r in rows if r in grp}
-        live = sum(1 for r in rows if r not in grp or size[grp[r]] > 1)   # single-row groups: dead rows
-        return live + sum(dcost(size[g]) for g in gs)
-
-    swept = sorted(colp[K:n - 1], key=cost)   # sorted() is stable
-    return list(colp[:K]) + swept + list(colp[n - 1:])
-
-
 def degree_sort_ascending(n: int, cptrs):
     """Sec. VI-B: columns by nonzero count ascending, ties by index."""
     return sorted(range(n), key=lambda j: (cptrs[j + 1] - cptrs[j], j))

@@ -361,3 +361,44 @@ def test_complex_band_dp_vs_naive_and_nw():
     v, sabs = oracle.perm_nw_complex(U)
     assert abs(b - v) <= 1e-14 * sabs
     assert abs(b - oracle.perm_naive_complex(U)) <= 1e-14 * sabs
+
+
+# ---- round 2: pins for the remaining oracle surfaces ---------------------------
+
+def test_nw2_zero_count_by_brute_force():
+    """nw2_range_exact's second output = number of Gray states g in the range
+    with some x_i(Gray_g) = 0 (the zero-tracking quantity of Sec. VI-B, P:589,
+    P:684).  Brute force over subsets S of columns 0..n-2, typed out from the
+    doubled form 2x_i(S) = 2a_{i,n-1} - r_i + 2 sum_{j in S} a_ij."""
+    for seed in (2, 3, 5):
+        A = synth.erdos_renyi(10, 0.3, seed, binary=True).astype(np.int64)
+        n = 10
+        r = A.sum(axis=1)
+        zeros_all = 0
+        for mask in range(1 << (n - 1)):
+            x2 = 2 * A[:, n - 1] - r + 2 * sum(A[:, j] for j in range(n - 1) if mask >> j & 1)
+            zeros_all += bool((x2 == 0).any())
+        T, z = oracle.nw2_range_exact(A, 0, 1 << (n - 1))
+        assert z == zeros_all                       # the Gray walk visits every subset once
+        # and over a sub-range: count the Gray codes g ^ (g >> 1) it visits
+        lo, hi = 37, 300
+        zr = 0
+        for g in range(lo, hi):
+            mask = g ^ (g >> 1)
+            x2 = 2 * A[:, n - 1] - r + 2 * sum(A[:, j] for j in range(n - 1) if mask >> j & 1)
+            zr += bool((x2 == 0).any())
+        assert oracle.nw2_range_exact(A, lo, hi)[1] == zr
+
+
+def test_nw_range_complex_additivity_and_scale():
+    rng = np.random.default_rng(11)
+    n = 8
+    A = (rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))) * (rng.uniform(size=(n, n)) < 0.6)
+    A += np.eye(n)
+    N = 1 << (n - 1)
+    total, _ = oracle.nw_range_complex(A, 0, N)
+    a, _ = oracle.nw_range_complex(A, 0, 41)
+    b, _ = oracle.nw_range_complex(A, 41, N)
+    assert abs((a + b) - total) <= 1e-12 * abs(total)
+    bp = brute_perm_c(A)
+    assert abs(total * (4 * (n % 2) - 2) - bp) <= 1e-12 * abs(bp)

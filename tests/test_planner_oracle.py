@@ -172,3 +172,26 @@ def test_alg4_region_invariant_and_ordering_trend(p):
         ks_ord.append(k)
         ks_raw.append(k_raw)
     assert np.mean(ks_ord) <= np.mean(ks_raw)   # Fig. 4 trend
+
+
+def test_gray_code_definition():
+    """Gray_g = g XOR (g >> 1): a bijection on [0, 2^k) whose
+    consecutive codes differ in exactly one bit, the bit ctz(g) (Alg. 1 line 9)."""
+    k = 10
+    codes = [P.gray(g) for g in range(1 << k)]
+    assert sorted(codes) == list(range(1 << k))
+    for g in range(1, 1 << k):
+        d = codes[g] ^ codes[g - 1]
+        assert d & (d - 1) == 0 and d == g & -g
+
+
+def test_degree_sort_properties():
+    """Sec. VI-B degree sort: a permutation whose column degrees are
+    nondecreasing, equal degrees in ascending index."""
+    A = synth.erdos_renyi(30, 0.2, 4)
+    cp, ri, _ = synth.to_ccs(A)
+    order = P.degree_sort_ascending(30, cp)
+    assert sorted(order) == list(range(30))
+    deg = [(A[:, j] != 0).sum() for j in order]
+    for a, b, da, db in zip(order, order[1:], deg, deg[1:]):
+        assert da < db or (da == db and a < b)

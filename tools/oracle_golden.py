@@ -4,7 +4,8 @@ long-double Alg. 1 permanent (oracle.perm_nw) and sum |terms|.
 
     python tools/oracle_golden.py [--names c3_n36,c4_n40]
 
-C4 (n=40, 2^39 Gray steps) takes ~40 min on 16 host cores; C3 (n=36) ~2.5 min.
+C4 (n=40, 2^39 Gray steps) takes ~40 min on 16 host cores; C3 (n=36) ~2.5 min;
+the exact 0/1 n=40 case (c4b_n40_01) ~2.5 h on 8 cores.
 """
 from __future__ import annotations
 
@@ -25,6 +26,12 @@ CASES = {
     "c4_n40": ("Erdos-Renyi n=40 p=0.2 seed=1, values U(0,1] (BASELINE configs[3], the bench workload)",
                lambda: synth.erdos_renyi(40, 0.2, 1)),
 }
+# exact integer goldens (0/1 inputs): oracle.perm_nw_exact = Alg. 1 in doubled
+# integers, wrapping int128, certified by T' = 0 mod 2^(n-1)
+EXACT_CASES = {
+    "c4b_n40_01": ("0/1 Erdos-Renyi n=40 p=0.2 seed=1 (the INT01 zero-skip workload, BASELINE configs[3] pattern)",
+                   lambda: synth.erdos_renyi(40, 0.2, 1, binary=True)),
+}
 
 
 def main():
@@ -32,6 +39,19 @@ def main():
     ap.add_argument("--names", default="c3_n36,c4_n40")
     a = ap.parse_args()
     for name in a.names.split(","):
+        if name in EXACT_CASES:
+            desc, make = EXACT_CASES[name]
+            A = make()
+            t0 = time.perf_counter()
+            v = oracle.perm_nw_exact(A)
+            dt = time.perf_counter() - t0
+            out = {"case": desc, "n": int(A.shape[0]), "perm_exact": str(v),
+                   "oracle": "oracle.perm_nw_exact (Alg. 1 in doubled exact integers, int128, T' divisible by 2^(n-1))",
+                   "seconds": round(dt, 1), "threads": oracle.max_threads(), "script": "tools/oracle_golden.py"}
+            path = os.path.join(ROOT, "tests", "golden", f"oracle_{name}.json")
+            json.dump(out, open(path, "w"), indent=1)
+            print(json.dumps(out), flush=True)
+            continue
         desc, make = CASES[name]
         A = make()
         t0 = time.perf_counter()
