@@ -11,6 +11,7 @@ Functions (each cites its passage; P:n = /root/reference/PAPER.md line n):
   perm_ryser_exact  Eq. 2, exact int128, integer inputs
   perm_nw           Alg. 1 + Sec. II-A chunking, long double
   nw_range          unscaled Alg. 1 partial sum over a Gray range (long double)
+  nw_range_f64      the same in IEEE double (CPU-baseline leg)
   nw2_range_exact   Alg. 1 in exact doubled integers (integer inputs)
   perm_band         band DP (exact textbook evaluation of Eq. 1 for banded A)
   structural_rank   maximum bipartite matching
@@ -64,6 +65,8 @@ def _load():
             L.oracle_perm_ryser_i128.argtypes = [ctypes.c_int, i64p, ctypes.c_int, u64p, u64p]
             L.oracle_nw_range_ld.argtypes = [ctypes.c_int, dp, ctypes.c_uint64, ctypes.c_uint64,
                                              ctypes.c_int, ldp, ldp]
+            L.oracle_nw_range_d.argtypes = [ctypes.c_int, dp, ctypes.c_uint64, ctypes.c_uint64,
+                                            ctypes.c_int, dp, dp]
             L.oracle_perm_nw_ld.restype = ctypes.c_longdouble
             L.oracle_perm_nw_ld.argtypes = [ctypes.c_int, dp, ctypes.c_int, ldp]
             L.oracle_nw2_range_i128.argtypes = [ctypes.c_int, i64p, ctypes.c_uint64, ctypes.c_uint64,
@@ -147,6 +150,15 @@ def nw_range(A, g_begin: int, g_end: int, threads: int = 0):
     _load().oracle_nw_range_ld(A.shape[0], _dp(A), g_begin, g_end, threads,
                                ctypes.byref(s), ctypes.byref(a))
     return float(s.value), float(a.value)
+
+
+def nw_range_f64(A, g_begin: int, g_end: int, threads: int = 0):
+    """nw_range in IEEE double (same chunking and fold): the FP64 analogue of
+    the paper's CPU-SparsePerman, used as a CPU baseline leg."""
+    A = _dense_f64(A)
+    s, a = ctypes.c_double(), ctypes.c_double()
+    _load().oracle_nw_range_d(A.shape[0], _dp(A), g_begin, g_end, threads, ctypes.byref(s), ctypes.byref(a))
+    return s.value, a.value
 
 
 def perm_nw(A, threads: int = 0):

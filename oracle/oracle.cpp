@@ -151,23 +151,27 @@ static void nw_prepare(NWMatrix& M, int n, const double* A) {
 static inline uint64_t gray(uint64_t g) { return g ^ (g >> 1); }
 
 // Sum over g in [gb, ge) of (-1)^g prod_i x_i(Gray_g); also sum of |terms|.
-static void nw_chunk(const NWMatrix& M, uint64_t gb, uint64_t ge, long double* out, long double* out_abs) {
+// R = long double (the oracle proper) or double (the FP64 CPU-SparsePerman
+// analogue timed as a CPU baseline; same steps, same order).
+extern "C++" {
+template <class R>
+static void nw_chunk(const NWMatrix& M, uint64_t gb, uint64_t ge, R* out, R* out_abs) {
     const int n = M.n;
-    long double x[64];
-    for (int i = 0; i < n; ++i) x[i] = M.x0[i];
+    R x[64];
+    for (int i = 0; i < n; ++i) x[i] = (R)M.x0[i];
     uint64_t G = gray(gb);
     for (int j = 0; j + 1 < n; ++j)
         if (G >> j & 1)
             for (int i : M.colrows[j]) x[i] += M.a[(size_t)i * n + j];
-    long double p = 0.0L, pa = 0.0L;
+    R p = 0, pa = 0;
     for (uint64_t g = gb; g < ge; ++g) {
         if (g != gb) {
             uint64_t d = gray(g) ^ gray(g - 1);
             int j = 63 - __builtin_clzll(d);                    // log2 of a power of two
-            long double s = 2.0L * (long double)(gray(g) >> j & 1) - 1.0L;
+            R s = (R)2 * (R)(gray(g) >> j & 1) - (R)1;
             for (int i : M.colrows[j]) x[i] += s * M.a[(size_t)i * n + j];
         }
-        long double prod = 1.0L;
+        R prod = 1;
         for (int i = 0; i < n; ++i) prod *= x[i];
         if (g & 1) p -= prod; else p += prod;
         pa += prod < 0 ? -prod : prod;
@@ -177,8 +181,9 @@ static void nw_chunk(const NWMatrix& M, uint64_t gb, uint64_t ge, long double* o
 }
 
 // pairwise (perfect binary tree on power-of-two lengths) sum in index order
-static long double pairwise(const long double* v, size_t len) {
-    if (len == 0) return 0.0L;
+template <class R>
+static R pairwise(const R* v, size_t len) {
+    if (len == 0) return 0;
     if (len == 1) return v[0];
     size_t h = 1;
     while (h * 2 < len) h *= 2;
@@ -187,8 +192,8 @@ static long double pairwise(const long double* v, size_t len) {
 
 // Unscaled NW sum over the Gray range [gb, ge):  sum (-1)^g prod_i x_i(Gray_g).
 // Chunks are the 2^12-aligned pieces of the range.  threads <= 0: all cores.
-void oracle_nw_range_ld(int n, const double* A, uint64_t gb, uint64_t ge, int threads,
-                        long double* out_sum, long double* out_abs) {
+template <class R>
+static void nw_range(int n, const double* A, uint64_t gb, uint64_t ge, int threads, R* out_sum, R* out_abs) {
     NWMatrix M;
     nw_prepare(M, n, A);
     const uint64_t CH = 1ull << ORACLE_CHUNK_LOG2;
@@ -202,9 +207,9 @@ void oracle_nw_range_ld(int n, const double* A, uint64_t gb, uint64_t ge, int th
     // Full chunks are processed in batches of 2^16 chunks; each batch is a
     // perfect pairwise tree over its chunks, batches are folded pairwise.
     const uint64_t BATCH = 1ull << 16;
-    std::vector<long double> batch_sum, batch_abs;
+    std::vector<R> batch_sum, batch_abs;
     int nt = threads > 0 ? threads : omp_get_max_threads();
-    std::vector<long double> cs, ca;
+    std::vector<R> cs, ca;
     for (uint64_t b0 = 0; b0 < nfull; b0 += BATCH) {
         uint64_t bn = std::min(BATCH, nfull - b0);
         cs.assign(bn, 0.0L);
@@ -217,9 +222,9 @@ void oracle_nw_range_ld(int n, const double* A, uint64_t gb, uint64_t ge, int th
         batch_sum.push_back(pairwise(cs.data(), bn));
         batch_abs.push_back(pairwise(ca.data(), bn));
     }
-    std::vector<long double> parts, parts_abs;
+    std::vector<R> parts, parts_abs;
     if (!pieces.empty()) {
-        long double s, a;
+        R s, a;
         nw_chunk(M, pieces[0].first, pieces[0].second, &s, &a);
         parts.push_back(s);
         parts_abs.push_back(a);
@@ -229,15 +234,29 @@ void oracle_nw_range_ld(int n, const double* A, uint64_t gb, uint64_t ge, int th
         parts_abs.push_back(pairwise(batch_abs.data(), batch_abs.size()));
     }
     if (tail_start < ge && tail_start >= first) {
-        long double s, a;
+        R s, a;
         nw_chunk(M, tail_start, ge, &s, &a);
         parts.push_back(s);
         parts_abs.push_back(a);
     }
-    long double S = 0.0L, SA = 0.0L;
+    R S = 0, SA = 0;
     for (size_t k = 0; k < parts.size(); ++k) { S += parts[k]; SA += parts_abs[k]; }
     *out_sum = S;
     *out_abs = SA;
+}
+
+}  // extern "C++"
+
+void oracle_nw_range_ld(int n, const double* A, uint64_t gb, uint64_t ge, int threads,
+                        long double* out_sum, long double* out_abs) {
+    nw_range<long double>(n, A, gb, ge, threads, out_sum, out_abs);
+}
+
+// The same sweep in IEEE double (x, products and sums): the FP64 analogue of
+// the paper's CPU-SparsePerman, a CPU baseline only.
+void oracle_nw_range_d(int n, const double* A, uint64_t gb, uint64_t ge, int threads,
+                       double* out_sum, double* out_abs) {
+    nw_range<double>(n, A, gb, ge, threads, out_sum, out_abs);
 }
 
 // perm(A) via Alg. 1 over the full range g in [0, 2^(n-1)), times the

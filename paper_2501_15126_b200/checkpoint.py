@@ -7,6 +7,7 @@ with perm_fold reproduces perm_compute bit for bit.
 """
 from __future__ import annotations
 
+import hashlib
 import json
 import os
 import struct
@@ -14,10 +15,24 @@ import struct
 from . import perm_result
 
 
+def _bits(x: float) -> int:
+    return struct.unpack("<Q", struct.pack("<d", x))[0]
+
+
+def _float(b: int) -> float:
+    return struct.unpack("<d", struct.pack("<Q", b))[0]
+
+
 def _key(plan, pieces: int) -> dict:
+    """Structure AND values: the generated kernel bakes every matrix value in
+    as a literal, so the hash of its source and cubin tells two matrices with
+    the same sparsity pattern apart (their partials must never be mixed)."""
     i = plan.info
+    h = hashlib.sha256(plan.source.encode())
+    h.update(plan.cubin())
     return {"n": i["n"], "nnz": i["nnz"], "K": i["K"], "B": i["B"], "M": i["M"], "tasks": i["tasks"],
-            "row_perm": i["row_perm"], "col_perm": i["col_perm"], "mode": i["mode"], "pieces": pieces}
+            "row_perm": i["row_perm"], "col_perm": i["col_perm"], "mode": i["mode"], "pieces": pieces,
+            "kernel_sha256": h.hexdigest()}
 
 
 def compute_resumable(plan, path: str, pieces: int = 256, max_pieces: int | None = None):
@@ -39,7 +54,7 @@ def compute_resumable(plan, path: str, pieces: int = 256, max_pieces: int | None
         if max_pieces is not None and swept >= max_pieces:
             return None
         s = plan.shard(r, pieces)
-        state["done"][str(r)] = {"bits": struct.unpack("<Q", struct.pack("<d", s.value))[0],
+        state["done"][str(r)] = {"bits": _bits(s.value), "bits_im": _bits(s.value_im),
                                  "lo": s.exact_lo, "hi": s.exact_hi, "valid": s.exact_valid,
                                  "sweep_ms": s.sweep_ms}
         tmp = path + ".tmp"
@@ -51,7 +66,8 @@ def compute_resumable(plan, path: str, pieces: int = 256, max_pieces: int | None
     for r in range(pieces):
         d = state["done"][str(r)]
         s = perm_result()
-        s.value = struct.unpack("<d", struct.pack("<Q", d["bits"]))[0]
+        s.value = _float(d["bits"])
+        s.value_im = _float(d["bits_im"])   # complex plans: imaginary partial (0 otherwise)
         s.exact_lo, s.exact_hi, s.exact_valid = d["lo"], d["hi"], d["valid"]
         s.sweep_ms = d["sweep_ms"]
         shards.append(s)

@@ -475,3 +475,97 @@ def test_full_size_permanent_vs_oracle_golden(name, n):
     for kw in ({}, {"autotune": -1}):
         v = plan(A, mode="reg", **kw).compute()
         assert rel(v, exp) < REL, (kw, v, exp, rel(v, exp))
+
+
+# ---- round 2: record-scale and untested-config parity ------------------------------
+
+def test_int01_er_n40_exact_vs_oracle_golden():
+    """0/1 ER n=40 p=0.2 (the INT01 zero-skip workload, DESIGN 3.9): the exact
+    permanent from the planner's pick (zero-aware placement, warp-task and block
+    zero skip) and from the plain zero-skip-off sweep against the exact
+    doubled-integer Alg. 1 oracle value (tests/golden/oracle_c4b_n40_01.json,
+    tools/oracle_golden.py, oracle only)."""
+    g = _golden("c4b_n40_01")
+    B = synth.erdos_renyi(40, 0.2, 1, binary=True)
+    exp = int(g["perm_exact"])
+    assert plan(B, mode="int01").exact() == exp
+    assert plan(B, mode="int01", autotune=-1).exact() == exp
+
+
+@pytest.mark.slow
+def test_record_scale_band54_vs_band_dp():
+    """Record-scale f3 workloads (2^53 Gray steps) against the exact band DP of
+    Eq. 1: real-orthogonal Givens brickwork (depth 4, the low-depth
+    boson-sampling shape), U(0,1] values on the same band, and the complex
+    unitary brickwork."""
+    A = synth.givens_brickwork(54, 4, 1)
+    exp = oracle.perm_band(A, synth.half_bandwidth(A))
+    assert rel(plan(A, mode="reg").compute(), exp) < REL
+    Bp = synth.band_positive(54, 4, 1)
+    exp = oracle.perm_band(Bp, synth.half_bandwidth(Bp))
+    assert rel(plan(Bp, mode="reg").compute(), exp) < REL
+    U = synth.unitary_brickwork(54, 4, 1)
+    exp = oracle.perm_band_complex(U, synth.half_bandwidth(U))
+    P = plan(U)
+    assert P.info["mode"] == 4
+    assert crel(P.compute(), exp) < REL
+
+
+@pytest.mark.slow
+def test_record_scale_er48_sampled_task_partials():
+    """ER n=48 p=0.2 (2^47 Gray steps, ~10 s on one B200): sampled per-task
+    partials against the oracle's long-double Alg. 1 partial over the same
+    Gray range."""
+    A = synth.erdos_renyi(48, 0.2, 1)
+    P = plan(A, mode="reg")
+    P.compute()
+    check_task_partials(A, P, 3)
+
+
+def test_plain_sweep_identity_order_n40_partials_vs_oracle():
+    """The literal Alg. 1 loop (no ordering, no eliminated columns,
+    factor_cols=-1) at n=40 p=0.2: the column order is the INPUT order, so the
+    sampled task partials are checked against oracle.nw_range on the input
+    matrix itself, with no product-chosen permutation in between."""
+    A = synth.erdos_renyi(40, 0.2, 1)
+    P = plan(A, ordering="none", mode="reg", factor_cols=-1)
+    i = P.info
+    assert i["K"] == 0 and i["col_perm"][:40] == list(range(40)) and i["row_perm"][:40] == list(range(40))
+    v = P.compute()
+    first, parts = P.task_partials()
+    L = 32 * i["M"] * (1 << i["B"])
+    rng = np.random.default_rng(1)
+    for t in sorted(set([0, len(parts) - 1] + rng.integers(0, len(parts), 3).tolist())):
+        exp, sabs = oracle.nw_range(A, (first + t) * L, (first + t + 1) * L)
+        assert abs(parts[t] - exp) <= 1e-11 * sabs, (t, parts[t], exp)
+    g = _golden("c4_n40")
+    assert rel(v, float(g["perm"])) < REL
+
+
+def test_hybrid_tier_n36_vs_oracle_golden():
+    """HYBRID with a populated tier (Alg. 4 split, Listing 4 layout) at the C3
+    size: whole permanent against the n=36 oracle golden."""
+    g = _golden("c3_n36")
+    A = synth.erdos_renyi(36, 0.2, 1)
+    P = plan(A, mode="hybrid", factor_cols=-1)
+    assert P.info["tier_rows"] > 0
+    assert rel(P.compute(), float(g["perm"])) < REL
+
+
+def test_checkpoint_resume_complex_and_value_keyed(tmp_path):
+    """Complex resumable runs keep the imaginary partials; a checkpoint of one
+    matrix is rejected for another matrix with the same sparsity pattern."""
+    from paper_2501_15126_b200.checkpoint import compute_resumable
+    U = synth.unitary_brickwork(28, 4, 2)
+    P = plan(U)
+    full = P.compute_ex()
+    ck = str(tmp_path / "c.json")
+    assert compute_resumable(P, ck, pieces=16, max_pieces=5) is None
+    r = compute_resumable(P, ck, pieces=16)
+    assert r.value == full.value and r.value_im == full.value_im and full.value_im != 0.0
+    A = synth.erdos_renyi(26, 0.25, 3)
+    A2 = A * 1.5
+    ck2 = str(tmp_path / "r.json")
+    assert compute_resumable(plan(A), ck2, pieces=16, max_pieces=3) is None
+    with pytest.raises(ValueError):
+        compute_resumable(plan(A2), ck2, pieces=16)

@@ -402,3 +402,20 @@ def test_nw_range_complex_additivity_and_scale():
     assert abs((a + b) - total) <= 1e-12 * abs(total)
     bp = brute_perm_c(A)
     assert abs(total * (4 * (n % 2) - 2) - bp) <= 1e-12 * abs(bp)
+
+
+def test_nw_range_f64_within_double_error_bound():
+    """The double-precision sweep (CPU-baseline leg) agrees with the long-double
+    oracle within u_double * (n + chunk depth) * sum|terms|, and is exact where
+    every x and product is a small dyadic rational (0/1 inputs: half-integers)."""
+    for seed in range(3):
+        A = synth.erdos_renyi(18, 0.3, seed)
+        N = 1 << 17
+        s_ld, a_ld = oracle.nw_range(A, 0, N)
+        s_d, a_d = oracle.nw_range_f64(A, 0, N)
+        assert abs(s_d - s_ld) <= 2.0 ** -53 * 64 * a_ld
+        assert abs(a_d - a_ld) <= 1e-12 * a_ld
+    B = synth.erdos_renyi(16, 0.3, 4, binary=True)
+    T, _ = oracle.nw2_range_exact(B, 0, 1 << 15)
+    s_d, _ = oracle.nw_range_f64(B, 0, 1 << 15)
+    assert s_d * 2 ** 16 == T          # x = x'/2 exact, products of <= 16 half-integers exact
