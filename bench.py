@@ -13,6 +13,11 @@ all-gathered with NCCL over NVLink, and perm_fold_async folds them in rank
 order and applies the Alg. 1 line-23 scale.  Time: CUDA events per step on the
 launching stream, barrier + synchronize around the timed region, max over ranks.
 L2 is flushed (256 MiB write) between timed steps (outside the step events).
+
+Besides `value` (the production plan, column elimination), the line carries
+`plain_sweep` (the literal Alg. 1 loop on the same matrix, its own roofline),
+`e2e` (public API from host arrays, warm caches) and `e2e_cold` (fresh
+processes: no caches; then the on-disk plan cache).
 """
 from __future__ import annotations
 
@@ -41,6 +46,8 @@ def parse():
     ap.add_argument("--p", type=float, default=DENSITY)
     ap.add_argument("--seed", type=int, default=SEED)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-plain", action="store_true", help="skip the plain Alg. 1 sweep leg")
+    ap.add_argument("--no-cold", action="store_true", help="skip the cold end-to-end leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ordering", default="auto")
     ap.add_argument("--mode", default="reg")
@@ -139,26 +146,61 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
+def host_info() -> dict:
+    """nproc, CPU model and SMT state of the host (cpu_baseline context)."""
+    out = {"nproc": os.cpu_count()}
+    try:
+        model, siblings, cores = None, None, None
+        for line in open("/proc/cpuinfo"):
+            k, _, v = line.partition(":")
+            k = k.strip()
+            if k == "model name" and model is None:
+                model = v.strip()
+            elif k == "siblings" and siblings is None:
+                siblings = int(v)
+            elif k == "cpu cores" and cores is None:
+                cores = int(v)
+        out["cpu_model"] = model
+        if siblings and cores:
+            out["threads_per_core"] = siblings // cores
+            out["smt"] = siblings > cores
+    except Exception:
+        pass
+    return out
+
+
 def cpu_baseline(A, target_s: float):
-    """The oracle as it stands (long-double Alg. 1, OpenMP over 2^12-step
-    chunks) on a bounded sample of the same Gray range, on all host cores."""
+    """The oracle as it stands on a bounded sample of the same Gray range, on
+    all host cores: the long-double Alg. 1 (the oracle proper) and the same
+    sweep in IEEE double (the FP64 analogue of the paper's CPU-SparsePerman,
+    P:589), each for about target_s / 2 seconds."""
     import oracle
     n = A.shape[0]
     total = 2 ** (n - 1)
     cores = oracle.max_threads()
-    probe = min(total, 1 << 22)
-    t0 = time.perf_counter()
-    oracle.nw_range(A, 0, probe)
-    rate = probe / max(time.perf_counter() - t0, 1e-6)
-    length = int(min(total, max(probe, rate * target_s)))
-    length = 1 << max(12, length.bit_length() - 1)
-    start = (total // 2) // length * length
-    t0 = time.perf_counter()
-    oracle.nw_range(A, start, start + length)
-    dt = time.perf_counter() - t0
-    return {"value": length / dt, "unit": "Gray-steps/s", "cores": cores, "kind": "oracle",
-            "sample": f"long-double Alg. 1 over Gray range [{start}, {start + length}) "
-                      f"= 2^{length.bit_length() - 1} of the 2^{n - 1} steps, {dt:.2f} s"}
+    legs = {}
+    for name, fn in (("f80", oracle.nw_range), ("f64", oracle.nw_range_f64)):
+        probe = min(total, 1 << 22)
+        t0 = time.perf_counter()
+        fn(A, 0, probe)
+        rate = probe / max(time.perf_counter() - t0, 1e-6)
+        length = int(min(total, max(probe, rate * target_s / 2)))
+        length = 1 << max(12, length.bit_length() - 1)
+        start = (total // 2) // length * length
+        t0 = time.perf_counter()
+        fn(A, start, start + length)
+        dt = time.perf_counter() - t0
+        legs[name] = {"value": length / dt, "seconds": dt, "gray_steps": length, "range": [start, start + length]}
+    f80 = legs["f80"]
+    return {"value": f80["value"], "unit": "Gray-steps/s", "cores": cores, "kind": "oracle",
+            "sample": f"long-double Alg. 1 over Gray range [{f80['range'][0]}, {f80['range'][1]}) "
+                      f"= 2^{f80['gray_steps'].bit_length() - 1} of the 2^{n - 1} steps, {f80['seconds']:.2f} s",
+            "f64_leg": {"value": legs["f64"]["value"], "unit": "Gray-steps/s",
+                        "what": "the same sweep in IEEE double (oracle.nw_range_f64): the FP64 CPU-SparsePerman "
+                                "analogue (P:589, P:623)",
+                        "sample": f"2^{legs['f64']['gray_steps'].bit_length() - 1} Gray steps, "
+                                  f"{legs['f64']['seconds']:.2f} s"},
+            "host": host_info()}
 
 
 def env_info(dev: int) -> dict:
@@ -230,6 +272,107 @@ def run_reference(args, rank, world):
           "e2e": {"value": value, "unit": "Gray-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
 
+def audited_kernel(info):
+    """ncu-audited executed DP instructions per Gray step and DRAM traffic per
+    launch of this exact kernel, from the committed `ncu` captures under
+    profiles/ (matched on the plan signature), else None."""
+    import glob
+    sig = {k: info[k] for k in ("n", "nnz", "K", "B", "U", "M", "tasks", "w_plan")}
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernel_ncu.json")), reverse=True):
+        for t in json.load(open(path)).get("entries", []):
+            if t.get("signature") == sig:
+                return t
+    return None
+
+
+def roofline(info, sweep_ms, gray_per_launch, peak, peak_def, peak_nominal):
+    """Roofline of the sweep kernel: FP64 lane-ops (DADD/DMUL/DFMA thread
+    instructions) per launch / launch time, against the FP64 lane peak."""
+    aud = audited_kernel(info)
+    w_ops, w_src = info["w_plan"], "generator count (W_plan)"
+    traffic, traffic_src = None, None
+    if aud:
+        traffic, traffic_src = aud.get("dram_bytes_per_launch"), aud.get("source")
+        if aud.get("w_exec"):
+            w_ops, w_src = aud["w_exec"], "ncu dadd+dmul+dfma thread-instructions / Gray steps"
+    achieved = w_ops * gray_per_launch / (sweep_ms / 1000.0) / 1e12
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "frac_of_nominal": achieved / peak_nominal, "peak_nominal": peak_nominal,
+            "traffic": traffic, "traffic_source": traffic_src,
+            "dp_ops_per_gray_step": w_ops, "dp_ops_source": w_src, "kernel": "perm_sweep (generated)",
+            "sweep_ms_avg": sweep_ms, "peak_def": peak_def,
+            "alg1_equiv_frac": info["w_alg1"] * gray_per_launch / (sweep_ms / 1000.0) / 1e12 / peak}
+
+
+def golden_rel_err(args, value):
+    """Relative error of the result against the committed oracle golden of the
+    same workload (tests/golden, written by tools/oracle_golden.py from oracle/
+    only), when one exists."""
+    path = os.path.join(ROOT, "tests", "golden", f"oracle_c4_n40.json")
+    if (args.n, args.p, args.seed) != (40, 0.2, 1) or not os.path.exists(path):
+        return None, None
+    g = json.load(open(path))
+    exp = float(g["perm"])
+    return abs(value - exp) / abs(exp), {"golden": g["perm"], "kappa": g["kappa"], "source": "tests/golden/oracle_c4_n40.json"}
+
+
+COLD_SCRIPT = r"""
+import json, sys, time
+sys.path.insert(0, {root!r})
+import numpy as np
+import synth
+t0 = time.perf_counter()
+import paper_2501_15126_b200 as pb
+A = synth.erdos_renyi({n}, {p}, {seed})
+ptr, idx, val = pb.dense_to_ccs(A)
+t1 = time.perf_counter()
+P = pb.Plan({n}, pb.PERM_CCS, ptr, idx, val, {ordering!r}, mode={mode!r}, device={dev}, autotune=-1)
+t2 = time.perf_counter()
+r = P.compute_ex()
+t3 = time.perf_counter()
+i = P.info
+print(json.dumps({{"plan_s": t2 - t1, "compute_s": t3 - t2, "e2e_s": t3 - t1, "value": r.value,
+                  "disk_cached": i["disk_cached"], "w_plan": i["w_plan"], "K": i["K"],
+                  "codegen_ms": i["codegen_ms"], "nvrtc_ms": i["nvrtc_ms"], "nvrtc_cpu_ms": i["nvrtc_cpu_ms"]}}))
+"""
+
+
+def e2e_cold(args, local):
+    """Cold end to end in fresh processes: the first perm_plan from host CCS
+    arrays with empty in-process caches (validation, ordering, searches,
+    codegen, NVRTC, module load) + compute + D2H.  Run twice with an empty
+    on-disk plan cache directory: the first run plans from scratch and fills
+    it, the second is a new process that finds the plan on disk."""
+    import shutil
+    import tempfile
+    d = tempfile.mkdtemp(prefix="perm_cache_")
+    out = {}
+    try:
+        for leg in ("no_cache", "disk_cache"):
+            code = COLD_SCRIPT.format(root=ROOT, n=args.n, p=args.p, seed=args.seed, ordering=args.ordering,
+                                      mode=args.mode, dev=local)
+            env = {**os.environ, "PERM_CACHE_DIR": d}
+            r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900, env=env)
+            lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+            out[leg] = json.loads(lines[-1]) if lines else {"error": r.stderr[-500:]}
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+    return out
+
+
+def time_steps(step, stream, steps, flush, dev_sync):
+    import torch
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    dev_sync()
+    for k in range(steps):
+        flush.zero_()
+        evs[k][0].record(stream)
+        step()
+        evs[k][1].record(stream)
+    dev_sync()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -239,20 +382,28 @@ def main():
         run_reference(args, rank, world)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2501_15126_b200 as pb
+    from paper_2501_15126_b200.dist import ShardedPermanent, init_comm, plan_on_rank0
 
     if args.same_device:
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group("gloo")
+    # a process group at every world size (N=1 included): it moves the NCCL
+    # unique id and the plan blob, and takes the max over ranks
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    if "MASTER_PORT" not in os.environ:
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+        sk.close()
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     A, cfg = workload(args)
     n = A.shape[0]
     steps_per_perm = 2 ** (n - 1) - 1
@@ -261,48 +412,61 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     kw = dict(mode=args.mode, device=local, stream=stream.cuda_stream, chunk_log2=args.chunk_log2,
-              block_log2=args.block_log2, task_chunks=args.task_chunks)
+              block_log2=args.block_log2, task_chunks=args.task_chunks, autotune=0 if args.autotune else -1)
     ptr, idx, val = pb.dense_to_ccs(A)
-    from paper_2501_15126_b200.dist import ShardedPermanent, agree_plan
-    if args.autotune:
-        plan, kw["autotune"] = agree_plan(
-            lambda **a: pb.Plan(n, pb.PERM_CCS, ptr, idx, val, args.ordering, **kw, **a), world)
+    t_plan0 = time.perf_counter()
+    if args.backend == "nccl":
+        # production path: libperm-owned NCCL communicator (a real collective
+        # even at N=1), rank-0 planning + plan broadcast, one async call per step
+        comm = init_comm(rank, world, local)
+        dkw = dict(rank=rank, world=world, nccl_comm=comm.handle)
+        plan = plan_on_rank0(lambda: pb.Plan(n, pb.PERM_CCS, ptr, idx, val, args.ordering, **kw, **dkw),
+                             rank, world, device=local, stream=stream.cuda_stream, **dkw)
+        out = torch.zeros(2, dtype=torch.float64, device=dev)
+        collective = f"NCCL all-gather of {8 if plan.partial_bytes == 8 else 16} B per rank inside libperm " \
+                     f"(perm_compute_async; libperm-owned communicator of {world} rank(s))"
+
+        def step_fn():
+            plan.compute_async(out.data_ptr())
     else:
-        kw["autotune"] = -1
+        # test path: ranks sharing one GPU (gloo host staging)
+        comm = None
         plan = pb.Plan(n, pb.PERM_CCS, ptr, idx, val, args.ordering, **kw)
+        sp = ShardedPermanent(plan, rank, world, dev)
+        out = sp.out
+        collective = "gloo host-staged all-gather (test path)"
+
+        def step_fn():
+            sp.step()
+    plan_wall_s = time.perf_counter() - t_plan0
     info = plan.info
-    sp = ShardedPermanent(plan, rank, world, dev)
-    out = sp.out
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step():
         # NVTX range: ncu captures of the bench (`--nvtx --nvtx-include bench_step/`)
         # see only the steps, not the planner's autotune sample launches
         torch.cuda.nvtx.range_push("bench_step")
-        sp.step()
+        step_fn()
         torch.cuda.nvtx.range_pop()
+
+    def sync_all():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     value0 = out[0].item()
 
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sweep_ms = []
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+
+    def timed_step():
+        step()
+        sweep_ms.append(plan.last_timing()[0])
+
     with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush.zero_()
-            evs[k][0].record(stream)
-            step()
-            evs[k][1].record(stream)
-            sweep_ms.append(plan.last_timing()[0])
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in evs]
+        step_ms = time_steps(timed_step, stream, args.steps, flush, sync_all)
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -313,23 +477,27 @@ def main():
     assert result == value0, "non-deterministic result"
 
     # ---- e2e: through the public C ABI from HOST buffers, every step:
-    # plan (host CCS -> validation, ordering, codegen, cubin (process cache),
-    # module upload) + shard sweep + NCCL all-gather + fold + D2H of the result.
+    # perm_plan (host CCS -> validation, structural rank, in-process planner
+    # cache, cached module, pooled buffers) + sweep + collective + fold + D2H
     e2e_ms = []
-    h2d = 0
     for k in range(args.steps + 1):
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+        sync_all()
         t0 = time.perf_counter()
-        P2 = pb.Plan(n, pb.PERM_CCS, ptr, idx, val, args.ordering, **kw)
-        s2 = ShardedPermanent(P2, rank, world, dev)
-        s2.step()
-        r = s2.value()
+        if args.backend == "nccl":
+            P2 = pb.Plan(n, pb.PERM_CCS, ptr, idx, val, args.ordering, **kw, rank=rank, world=world,
+                         nccl_comm=comm.handle) if rank == 0 else pb.Plan.from_blob(
+                             plan.export(), device=local, stream=stream.cuda_stream, rank=rank, world=world,
+                             nccl_comm=comm.handle)
+            r = P2.compute_ex().value
+        else:
+            P2 = pb.Plan(n, pb.PERM_CCS, ptr, idx, val, args.ordering, **kw)
+            s2 = ShardedPermanent(P2, rank, world, dev)
+            s2.step()
+            r = s2.value()
         dt = time.perf_counter() - t0
         cubin_bytes = len(P2.cubin())
         P2.close()
-        assert r == result
+        assert r == result, (r, result)
         if k > 0:
             e2e_ms.append(dt * 1000.0)
     t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
@@ -337,73 +505,108 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = steps_per_perm * len(e2e_ms) / (t.item() / 1000.0)
 
+    # ---- the literal Alg. 1 loop on the same matrix (no eliminated columns,
+    # factor_cols = -1): its own timing and roofline
+    plain = None
+    if not args.no_plain:
+        pkw = {**kw, "factor_cols": -1}
+        P0 = pb.Plan(n, pb.PERM_CCS, ptr, idx, val, "permanent", **pkw)
+        out0 = torch.zeros(2, dtype=torch.float64, device=dev)
+        for _ in range(3):
+            P0.shard_async(rank, world, out0.data_ptr())
+        psweep = []
+
+        def pstep():
+            torch.cuda.nvtx.range_push("plain_step")
+            P0.shard_async(rank, world, out0.data_ptr())
+            torch.cuda.nvtx.range_pop()
+            psweep.append(P0.last_timing()[0])
+        pms = time_steps(pstep, stream, max(3, args.steps // 4), flush, sync_all)
+        plain = (P0, pms, psweep)
+
     if rank == 0:
         clocks = clk.summary()
         sw = sum(sweep_ms) / len(sweep_ms)
         # Gray steps one sweep launch covers (h-steps x 2^K)
-        products = ((info["tasks"] // world if info["tasks"] >= world else 1) * 32 * info["M"]
-                    * (1 << info["B"]) << info["K"])
-        w_ops, w_src = info["w_plan"], "generator count (W_plan)"
+        def gray_per_launch(i):
+            return ((i["tasks"] // world if i["tasks"] >= world else 1) * 32 * i["M"] * (1 << i["B"]) << i["K"])
+        products = gray_per_launch(info)
         sm_max = clocks.get("sm_max_mhz") or 1965.0
-        peak = info["sms"] * 64 * sm_max * 1e6 / 1e12
-        # DRAM traffic per launch from the committed `ncu --set full` capture of
-        # this same kernel (profiles/), when the plan signature matches
-        traffic, traffic_src = None, None
-        tpath = os.path.join(ROOT, "profiles", "r1_bench_kernel_ncu.json")
-        if os.path.exists(tpath):
-            sig = {k: info[k] for k in ("n", "nnz", "K", "B", "U", "M", "tasks", "w_plan")}
-            for t in json.load(open(tpath)).get("entries", []):  # one entry per audited plan
-                if t.get("signature") != sig:
-                    continue
-                traffic, traffic_src = t["dram_bytes_per_launch"], t["source"]
-                if t.get("w_exec"):
-                    # nvcc's own CSE across the switch join removes ~3 % of the
-                    # generated DP instructions: count what executes (ncu)
-                    w_ops, w_src = t["w_exec"], "ncu dadd+dmul+dfma thread-instructions / Gray steps"
-        achieved = w_ops * products / (sw / 1000.0) / 1e12
+        peak_nominal = info["sms"] * 64 * sm_max * 1e6 / 1e12
+        try:
+            mp, mp_ms = pb.perm_probe_fp64_peak(local)
+            peak = mp / 1e12
+            peak_def = (f"measured: FP64 DFMA-chain probe (perm_probe_fp64_peak, {mp_ms:.2f} ms best of 5) on this "
+                        f"GPU = {peak:.3f} T lane-ops/s; 1 op per DADD/DMUL/DFMA thread-instruction; nominal "
+                        f"{info['sms']} SMs x 64 FP64 lanes x {sm_max:.0f} MHz = {peak_nominal:.3f}")
+        except Exception as e:  # noqa: BLE001
+            peak, peak_def = peak_nominal, f"nominal {info['sms']} SMs x 64 FP64 lanes x {sm_max:.0f} MHz (probe failed: {e})"
+        rf = roofline(info, sw, products, peak, peak_def, peak_nominal)
+        rel_err, golden = golden_rel_err(args, result)
         line = {
             "metric": "gray_steps_per_s", "value": value, "unit": "Gray-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
             "sec_per_permanent": ms_per_step / 1000.0,
             "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": value / PAPER_STEPS_PER_S, "dtype": "f64", "data": "synthetic",
-            "config": {**cfg, "parallelism": f"gray-range shards x{world}, NCCL all-gather of 8 B",
+            "vs_baseline": value / PAPER_STEPS_PER_S,
+            "vs_baseline_note": "= paper A100 CodeGen-Hybrid sec/permanent (3.94 s, n=40 p=0.2, P:627) / ours: "
+                                "algorithm (column elimination, DESIGN 3.6) AND hardware differ; context only",
+            "dtype": "f64", "data": "synthetic",
+            "config": {**cfg, "parallelism": f"gray-range shards x{world}; {collective}",
                        "l2": "inputs <= 5 KB (baked into the generated kernel); 256 MiB L2 flush between steps",
                        "ordering": ["none", "degree", "permanent", "auto"][info["ordering"]],
                        "mode": ["auto", "reg", "hybrid", "int01"][info["mode"]],
                        "B": info["B"], "U": info["U"], "M": info["M"], "tasks": info["tasks"],
+                       "k": info["k"], "c": info["c"],
                        "regs": info["regs_per_thread"], "grid": info["grid"], "block": info["block"],
                        "w_plan_fp64_ops_per_step": info["w_plan"], "w_alg1_ops_per_step": info["w_alg1"],
                        "K": info["K"], "plan_choice": "autotune" if kw["autotune"] == 0 else "model",
-                       "vs_baseline_ref": "paper CodeGen-Hybrid A100 n=40 p=0.2: 3.94 s (P:627), context only"},
-            "result": result,
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "dp_ops_per_gray_step": w_ops, "dp_ops_source": w_src,
-                         "kernel": "perm_sweep (generated)", "sweep_ms_avg": sw,
-                         "peak_def": f"{info['sms']} SMs x 64 FP64 lanes x {sm_max:.0f} MHz, 1 op per "
-                                     "DADD/DMUL/DFMA lane-op (datasheet FP64 / 2)",
-                         "alg1_equiv_frac": info["w_alg1"] * products / (sw / 1000.0) / 1e12 / peak},
+                       "plan_source": "rank 0 planned, blob broadcast to the other ranks" if world > 1 else "planned"},
+            "result": result, "rel_err": rel_err, "rel_err_ref": golden,
+            "h_steps_per_s": value / (1 << info["K"]),
+            "executed_dp_ops_per_s": rf["dp_ops_per_gray_step"] * products / (sw / 1000.0),
+            "roofline": rf,
             "clocks": clocks,
             "env": env_info(local),
             "e2e": {"value": e2e_value, "unit": "Gray-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 8,
-                    "what": "perm_plan from the host CCS arrays every step (validation, structural rank, planner-cache "
-                            "lookup; cached library and pooled buffers after the first call) + sweep + all-gather + "
-                            "fold + D2H of the 8-byte result, wall clock, max over ranks",
+                    "what": "perm_plan from the host CCS arrays every step (validation, structural rank, in-process "
+                            "planner-cache hit; cached module, pooled buffers) + sweep + collective + fold + D2H of "
+                            "the 8-byte result, wall clock, max over ranks",
                     "input_path": f"the matrix values reach the device as literals of the generated kernel: its "
                                   f"{cubin_bytes}-byte cubin is uploaded once per distinct matrix (first call), so no "
                                   f"per-step H2D data copy exists"},
             "gpu_launches": launches_per_step(info["tasks"] // max(1, world) if info["tasks"] >= world else 1)
                             * args.steps,
-            "plan_ms": info["plan_ms"], "nvrtc_ms": info["nvrtc_ms"],
+            "plan_ms": info["plan_ms"], "plan_wall_s": plan_wall_s,
+            "plan_phases_ms": {"codegen": info["codegen_ms"], "nvrtc_wall": info["nvrtc_ms"],
+                               "nvrtc_cpu": info["nvrtc_cpu_ms"], "autotune": info["autotune_ms"],
+                               "candidates_compiled": info["candidates_compiled"]},
         }
+        if plain is not None:
+            P0, pms, psweep = plain
+            i0 = P0.info
+            psw = sum(psweep) / len(psweep)
+            prf = roofline(i0, psw, gray_per_launch(i0), peak, peak_def, peak_nominal)
+            pms_avg = sum(pms) / len(pms)
+            line["plain_sweep"] = {
+                "what": "the literal Alg. 1 loop (P:86-115) on the same matrix: Alg. 3 ordering, factor_cols=-1 "
+                        "(no eliminated columns), same geometry rules, same event/flush discipline",
+                "ms_per_step": pms_avg, "value": steps_per_perm / (pms_avg / 1000.0), "unit": "Gray-steps/s",
+                "K": i0["K"], "B": i0["B"], "U": i0["U"], "regs": i0["regs_per_thread"],
+                "w_plan": i0["w_plan"], "w_alg1": i0["w_alg1"], "roofline": prf}
+            P0.close()
+        if not args.no_cold:
+            line["e2e_cold"] = e2e_cold(args, local)
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(A, args.cpu_seconds)
         emit(line)
+    plan.close()
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.barrier()
-        dist.destroy_process_group()
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -53,7 +53,7 @@ typedef enum {
   PERM_ENOMEM = 3,  /* host or device allocation failed */
   PERM_ECUDA = 4,   /* CUDA runtime error / no sm_100 device */
   PERM_ENVRTC = 5,  /* NVRTC compilation failed */
-  PERM_ENCCL = 6,   /* reserved: collective failure */
+  PERM_ENCCL = 6,   /* NCCL unavailable or a collective failed */
   PERM_ESPILL = 7   /* generated kernel spills to local memory (register budget) */
 } perm_status;
 
@@ -92,7 +92,19 @@ typedef struct {
                             strided sample of their task range and keep a clearly
                             (>4 %) faster one over the model's pick; -1 = off
                             (the model's pick: deterministic across processes) */
-  int reserved[4];
+  int rank, world;       /* multi-GPU: perm_compute / _ex / _async sweep
+                            shard `rank` of `world` (power of two) and all-gather the
+                            partials over nccl_comm; world 0 or 1 = one GPU */
+  int reseed_log2;       /* R: x is re-seeded exactly from x0 at least every 2^R swept
+                            steps (Sec. II-A seeding; bounds FP64 drift, SURVEY
+                            8(c)).  Every chunk is seeded exactly, so this caps the
+                            chunk: B <= R.  0 = auto (B) */
+  int reserved0;
+  void *nccl_comm;       /* ncclComm_t over the `world` ranks (perm_comm_init, or the
+                            caller's from the same libnccl.so.2 instance); borrowed */
+  const char *cache_dir; /* on-disk plan cache directory (plan files named by a hash of
+                            matrix + options + library build); NULL = $PERM_CACHE_DIR,
+                            unset = no disk cache.  Read at perm_plan time only */
 } perm_opts;
 
 /* Result of a computation. */
@@ -106,6 +118,14 @@ typedef struct {
   double sweep_ms;       /* device time of the sweep kernel (CUDA events) */
   double reduce_ms;      /* device time of the deterministic reduction */
   double value_im;       /* complex plans: imaginary part of `value` (else 0) */
+  uint64_t steps;        /* Gray steps of Alg. 1 this result covers (= products) */
+  double seconds;        /* device seconds of sweep + reduction (+ fold / collective) */
+  double w_plan;         /* the plan's FP64 (INT01: integer) ops per Gray step */
+  int k, c;              /* Alg. 4 partition of the base ordering */
+  int b;                 /* B, chunk log2 (Lemma 1) */
+  int mode;              /* perm_mode of the kernel that ran */
+  int K;                 /* eliminated columns (DESIGN 3.6) */
+  int reserved_r;
 } perm_result;
 
 /* Plan inspection (all indices refer to the ORDERED matrix unless noted). */
@@ -139,12 +159,20 @@ typedef struct {
   int regs_per_thread, local_bytes;
   int smem_bytes;         /* dynamic shared memory per block: loop-carried values the
                              unrolled block body never references (per-thread slots) */
-  double plan_ms, codegen_ms, nvrtc_ms;
+  double plan_ms;         /* wall time of perm_plan (all phases below + device setup) */
+  double codegen_ms;      /* wall: ordering + elimination searches + candidate codegen */
+  double nvrtc_ms;        /* wall: concurrent NVRTC compiles of the kept candidates */
   int cubin_cached;       /* 1 if the cubin came from the in-process cache */
   int plan_cached;        /* 1 if ordering/codegen/NVRTC came from the in-process
                              planner cache (same CCS content and options) */
   int row_perm[64];       /* ordered row i = original row row_perm[i] */
   int col_perm[64];       /* ordered column j = original column col_perm[j] */
+  double autotune_ms;     /* wall: on-device timing of the compiled candidates */
+  double nvrtc_cpu_ms;    /* sum of the individual NVRTC compile times (> nvrtc_ms when
+                             candidates compile concurrently) */
+  int disk_cached;        /* 1 if the planning output came from the on-disk plan cache
+                             or from perm_plan_import */
+  int candidates_compiled;
 } perm_plan_info;
 
 /* ---- plan / compute / free (north-star surface) ------------------------ */
@@ -167,10 +195,23 @@ int perm_plan_complex(int n, perm_format fmt, const int32_t *ptr, const int32_t 
                       const double *val_re_im, perm_ordering ord, const perm_opts *opts,
                       perm_plan_t *out);
 
-/* perm(A) on one GPU (whole Gray range).  NaN on error (see perm_last_error).
- * Synchronises the plan's stream. */
+/* perm(A).  One GPU (opts.world <= 1): the whole Gray range.  Multi-GPU
+ * (opts.world > 1, opts.nccl_comm set): this rank sweeps shard opts.rank, the
+ * partials are all-gathered over NCCL on the plan's stream and folded in rank
+ * order -- every rank returns the same bits as a one-GPU run.  NaN on error
+ * (see perm_last_error).  Synchronises the plan's stream. */
 double perm_compute(perm_plan_t p);
 int perm_compute_ex(perm_plan_t p, perm_result *r);
+
+/* Asynchronous perm_compute on the plan's stream: writes perm(A) (8 bytes FP64,
+ * 16 bytes complex (re, im) or INT01 int128) to the DEVICE pointer d_out; no
+ * host synchronisation (sweep -> tree -> [all-gather] -> fold, all enqueued). */
+int perm_compute_async(perm_plan_t p, void *d_out);
+
+/* SURVEY 8(b) surface: UNSCALED partial of shard `rank` of `world` to host
+ * memory -- 1 double (FP64; INT01: the exact T' partial rounded to double, use
+ * perm_compute_shard for the exact bits), 2 doubles (re, im) for complex plans. */
+int perm_compute_partial(perm_plan_t p, int rank, int world, double *partial);
 
 /* Shard `rank` of `world` (world a power of two; Sec. 8(e) Gray-range
  * sharding): r->value = UNSCALED partial sum over this shard's contiguous,
@@ -225,6 +266,31 @@ const char *perm_plan_source(perm_plan_t p);
 int perm_plan_cubin(perm_plan_t p, void *buf, size_t *size);
 
 void perm_free(perm_plan_t p); /* NULL-safe */
+
+/* ---- plan transport: on-disk cache and rank-0 broadcast ----------------
+ * perm_plan_export serialises a plan's planning output (validated matrix,
+ * orderings, kernel spec and source, sm_100a cubin, info) to buf; *size in:
+ * capacity, out: bytes needed/copied (call with buf = NULL to size).
+ * perm_plan_import builds a plan from such a blob (from the same libperm build;
+ * PERM_EINVAL otherwise) without re-planning: no search, no NVRTC -- the device
+ * part (module load, buffers) follows `opts` (device, stream, rank/world/comm,
+ * no_device).  Multi-GPU runs plan on rank 0 and broadcast the blob so every
+ * rank runs the same kernel bits. */
+int perm_plan_export(perm_plan_t p, void *buf, size_t *size);
+int perm_plan_import(const void *blob, size_t size, const perm_opts *opts, perm_plan_t *out);
+
+/* ---- NCCL communicator owned by libperm (dlopen'd libnccl.so.2) ---------
+ * Rank 0 calls perm_comm_unique_id, ships the 128 bytes to every rank (e.g.
+ * over torch.distributed), each rank calls perm_comm_init (collective: all
+ * ranks must call it) and passes the comm as perm_opts.nccl_comm. */
+int perm_comm_unique_id(void *id128);
+int perm_comm_init(int world, int rank, const void *id128, int device, void **comm);
+int perm_comm_destroy(void *comm);
+
+/* Measured FP64 lane-op throughput of `device` (DFMA chains at full occupancy;
+ * one DADD/DMUL/DFMA thread-instruction = one op): the roofline denominator of
+ * the sweep.  *ms = best kernel time. */
+int perm_probe_fp64_peak(int device, double *lane_ops_per_s, double *ms);
 
 const char *perm_last_error(void);
 const char *perm_version(void);

@@ -18,7 +18,9 @@ import numpy as np
 from . import _abi
 from ._abi import MODE, ORDER, PERM_CCS, PERM_CRS, STATUS, perm_opts, perm_plan_info, perm_result
 
-__all__ = ["PermError", "Plan", "perm_plan", "perm_compute", "perm_compute_ex", "perm_compute_shard",
+__all__ = ["PermError", "Plan", "Comm", "perm_plan", "perm_compute", "perm_compute_ex", "perm_compute_shard",
+           "perm_compute_async", "perm_compute_partial", "perm_plan_export", "perm_plan_import",
+           "perm_probe_fp64_peak",
            "perm_fold", "perm_free", "perm_structural_rank", "perm_order", "perm_partition",
            "perm_alg2_launch_parameters", "dense_to_ccs", "dense_to_crs", "perm_version"]
 
@@ -66,8 +68,14 @@ def dense_to_crs(A):
 
 def make_opts(mode="auto", device=0, stream=None, chunk_log2=0, block_log2=0, task_chunks=0,
               gr_ratio=0.0, hybrid_c=0, threads_per_block=0, no_device=False, factor_cols=0,
-              min_blocks=0, zero_skip=0, autotune=0) -> perm_opts:
+              min_blocks=0, zero_skip=0, autotune=0, rank=0, world=0, reseed_log2=0, nccl_comm=None,
+              cache_dir=None) -> perm_opts:
     o = perm_opts()
+    o.rank = rank
+    o.world = world
+    o.reseed_log2 = reseed_log2
+    o.nccl_comm = nccl_comm.handle if isinstance(nccl_comm, Comm) else nccl_comm
+    o.cache_dir = cache_dir.encode() if isinstance(cache_dir, str) else cache_dir
     o.autotune = autotune
     o.factor_cols = factor_cols
     o.min_blocks = min_blocks
@@ -139,6 +147,60 @@ def perm_fold_async(h, d_partials: int, world: int, d_out: int):
            "perm_fold_async")
 
 
+def perm_compute_async(h, d_out: int):
+    _check(_abi.lib().perm_compute_async(h, ctypes.c_void_p(d_out)), "perm_compute_async")
+
+
+def perm_compute_partial(h, rank: int, world: int):
+    buf = (ctypes.c_double * 2)()
+    _check(_abi.lib().perm_compute_partial(h, rank, world, buf), "perm_compute_partial")
+    return buf[0], buf[1]
+
+
+def perm_plan_export(h) -> bytes:
+    L = _abi.lib()
+    sz = ctypes.c_size_t(0)
+    _check(L.perm_plan_export(h, None, ctypes.byref(sz)), "perm_plan_export")
+    buf = ctypes.create_string_buffer(sz.value)
+    _check(L.perm_plan_export(h, buf, ctypes.byref(sz)), "perm_plan_export")
+    return buf.raw[: sz.value]
+
+
+def perm_plan_import(blob: bytes, opts: perm_opts | None = None) -> int:
+    h = ctypes.c_void_p()
+    _check(_abi.lib().perm_plan_import(blob, len(blob), ctypes.byref(opts or make_opts()), ctypes.byref(h)),
+           "perm_plan_import")
+    return h.value
+
+
+def perm_probe_fp64_peak(device: int = 0):
+    """Measured FP64 lane-ops/s of `device` and the best kernel ms (perm.h)."""
+    v, ms = ctypes.c_double(), ctypes.c_double()
+    _check(_abi.lib().perm_probe_fp64_peak(device, ctypes.byref(v), ctypes.byref(ms)), "perm_probe_fp64_peak")
+    return v.value, ms.value
+
+
+class Comm:
+    """NCCL communicator owned by libperm (perm_comm_init); rank 0's 128-byte
+    unique id must reach every rank first (comm_unique_id + any transport)."""
+
+    def __init__(self, world: int, rank: int, uid: bytes, device: int = 0):
+        h = ctypes.c_void_p()
+        _check(_abi.lib().perm_comm_init(world, rank, uid, device, ctypes.byref(h)), "perm_comm_init")
+        self.handle, self.world, self.rank = h.value, world, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(_abi.lib().perm_comm_unique_id(buf), "perm_comm_unique_id")
+        return buf.raw
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _check(_abi.lib().perm_comm_destroy(self.handle), "perm_comm_destroy")
+            self.handle = None
+
+
 def perm_free(h):
     if h:
         _abi.lib().perm_free(h)
@@ -194,7 +256,28 @@ class Plan:
     def __init__(self, n, fmt, ptr, idx, val, ordering="auto", **opts):
         self.n = int(n)
         self.is_complex = bool(np.iscomplexobj(val))
-        self.handle = perm_plan(self.n, fmt, ptr, idx, val, ordering, make_opts(**opts))
+        self._opts = make_opts(**opts)   # kept alive: cache_dir / comm pointers
+        self.handle = perm_plan(self.n, fmt, ptr, idx, val, ordering, self._opts)
+
+    @classmethod
+    def from_blob(cls, blob: bytes, **opts):
+        """Plan from a perm_plan_export blob (no search, no NVRTC)."""
+        self = cls.__new__(cls)
+        self._opts = make_opts(**opts)
+        self.handle = perm_plan_import(blob, self._opts)
+        self.n = self.info["n"]
+        self.is_complex = self.info["mode"] == 4
+        return self
+
+    def export(self) -> bytes:
+        return perm_plan_export(self.handle)
+
+    def compute_async(self, d_out: int):
+        perm_compute_async(self.handle, d_out)
+
+    def compute_partial(self, rank: int, world: int):
+        re, im = perm_compute_partial(self.handle, rank, world)
+        return complex(re, im) if self.is_complex else re
 
     @classmethod
     def from_dense(cls, A, ordering="auto", fmt=PERM_CCS, **opts):

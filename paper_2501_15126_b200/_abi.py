@@ -24,14 +24,18 @@ class perm_opts(ctypes.Structure):
                 ("gr_ratio", ctypes.c_double), ("hybrid_c", ctypes.c_int),
                 ("threads_per_block", ctypes.c_int), ("no_device", ctypes.c_int),
                 ("factor_cols", ctypes.c_int), ("min_blocks", ctypes.c_int), ("zero_skip", ctypes.c_int),
-                ("autotune", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
+                ("autotune", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
+                ("reseed_log2", ctypes.c_int), ("reserved0", ctypes.c_int), ("nccl_comm", ctypes.c_void_p),
+                ("cache_dir", ctypes.c_char_p)]
 
 
 class perm_result(ctypes.Structure):
     _fields_ = [("value", ctypes.c_double), ("exact_lo", ctypes.c_uint64), ("exact_hi", ctypes.c_uint64),
                 ("exact_valid", ctypes.c_int), ("world", ctypes.c_int), ("rank", ctypes.c_int),
                 ("products", ctypes.c_uint64), ("sweep_ms", ctypes.c_double), ("reduce_ms", ctypes.c_double),
-                ("value_im", ctypes.c_double)]
+                ("value_im", ctypes.c_double), ("steps", ctypes.c_uint64), ("seconds", ctypes.c_double),
+                ("w_plan", ctypes.c_double), ("k", ctypes.c_int), ("c", ctypes.c_int), ("b", ctypes.c_int),
+                ("mode", ctypes.c_int), ("K", ctypes.c_int), ("reserved_r", ctypes.c_int)]
 
     def complex_value(self) -> complex:
         return complex(self.value, self.value_im)
@@ -53,7 +57,9 @@ class perm_plan_info(ctypes.Structure):
                 ("blocks_per_sm", ctypes.c_int), ("sms", ctypes.c_int), ("regs_per_thread", ctypes.c_int),
                 ("local_bytes", ctypes.c_int), ("smem_bytes", ctypes.c_int), ("plan_ms", ctypes.c_double),
                 ("codegen_ms", ctypes.c_double), ("nvrtc_ms", ctypes.c_double), ("cubin_cached", ctypes.c_int), ("plan_cached", ctypes.c_int),
-                ("row_perm", ctypes.c_int * 64), ("col_perm", ctypes.c_int * 64)]
+                ("row_perm", ctypes.c_int * 64), ("col_perm", ctypes.c_int * 64),
+                ("autotune_ms", ctypes.c_double), ("nvrtc_cpu_ms", ctypes.c_double), ("disk_cached", ctypes.c_int),
+                ("candidates_compiled", ctypes.c_int)]
 
     def as_dict(self):
         d = {}
@@ -70,7 +76,8 @@ EXPORTS = ["perm_plan", "perm_plan_ex", "perm_compute", "perm_compute_ex", "perm
            "perm_debug_task_partials", "perm_last_timing", "perm_plan_get_info", "perm_plan_source", "perm_plan_cubin",
            "perm_free", "perm_last_error", "perm_version", "perm_structural_rank", "perm_order",
            "perm_partition", "perm_alg2_launch_parameters", "perm_shard_range", "perm_fold_host",
-           "perm_plan_complex"]
+           "perm_plan_complex", "perm_compute_async", "perm_compute_partial", "perm_plan_export",
+           "perm_plan_import", "perm_comm_unique_id", "perm_comm_init", "perm_comm_destroy", "perm_probe_fp64_peak"]
 
 _lib = None
 
@@ -120,5 +127,13 @@ def lib():
     L.perm_shard_range.argtypes = [P, ctypes.c_int, ctypes.c_int, u64p, u64p, u64p, u64p]
     L.perm_fold_host.restype = ctypes.c_double
     L.perm_fold_host.argtypes = [P, dp, ctypes.c_int]
+    L.perm_compute_async.argtypes = [P, ctypes.c_void_p]
+    L.perm_compute_partial.argtypes = [P, ctypes.c_int, ctypes.c_int, dp]
+    L.perm_plan_export.argtypes = [P, ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t)]
+    L.perm_plan_import.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(perm_opts), ctypes.POINTER(P)]
+    L.perm_comm_unique_id.argtypes = [ctypes.c_void_p]
+    L.perm_comm_init.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(P)]
+    L.perm_comm_destroy.argtypes = [P]
+    L.perm_probe_fp64_peak.argtypes = [ctypes.c_int, dp, dp]
     _lib = L
     return L

@@ -200,21 +200,6 @@ Csx permute_ccs(const Csx& ccs, const std::vector<int>& rowp, const std::vector<
   return o;
 }
 
-std::vector<int> factor_picks(const Csx& ccs, const std::vector<int>& base_colp, int kmax) {
-  const int n = ccs.n;
-  std::vector<int> picks;
-  std::vector<char> used(n, 0);
-  for (int q = 0; q + 1 < n && (int)picks.size() < kmax; ++q) {
-    const int c = base_colp[q];
-    bool disjoint = ccs.ptr[c + 1] > ccs.ptr[c];
-    for (int p = ccs.ptr[c]; p < ccs.ptr[c + 1] && disjoint; ++p) disjoint = !used[ccs.idx[p]];
-    if (!disjoint) continue;
-    for (int p = ccs.ptr[c]; p < ccs.ptr[c + 1]; ++p) used[ccs.idx[p]] = 1;
-    picks.push_back(c);
-  }
-  return picks;
-}
-
 std::vector<int> factored_columns(const std::vector<int>& base_colp, const std::vector<int>& picks, int K) {
   std::vector<int> out(picks.begin(), picks.begin() + K);
   for (int c : base_colp)

@@ -36,9 +36,6 @@ void order_permanent(const Csx& ccs, const Csx& crs, std::vector<int>& rowp, std
 void order_degree(const Csx& ccs, std::vector<int>& rowp, std::vector<int>& colp);
 // ordered(i, j) = a(rowp[i], colp[j]); returns CCS of the ordered matrix
 Csx permute_ccs(const Csx& ccs, const std::vector<int>& rowp, const std::vector<int>& colp);
-// Factored columns (DESIGN "Factored columns"): greedy pairwise row-disjoint
-// picks among base_colp[0..n-2] in base order, at most kmax.
-std::vector<int> factor_picks(const Csx& ccs, const std::vector<int>& base_colp, int kmax);
 // column order with the first K picks moved to the front (pick order), the
 // other columns in base order (the base's last column stays last).
 std::vector<int> factored_columns(const std::vector<int>& base_colp, const std::vector<int>& picks, int K);

@@ -16,13 +16,22 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include "perm_internal.h"
+#include "plan_state.h"
 
 extern "C" cudaError_t libperm_launch_tree_reduce(const void* slots, uint64_t count, int kind, void* out,
                                                   void* scratch, cudaStream_t st);
 extern "C" size_t libperm_tree_scratch_bytes(uint64_t count, int kind);
 extern "C" cudaError_t libperm_launch_fold(const void* partials, int world, int n, int kind, int neg,
                                            void* out, cudaStream_t st);
+extern "C" cudaError_t libperm_probe_fp64_peak(int device, int reps, double* ops_per_s, double* ms_best);
+// collective.cpp (dlopen'd NCCL)
+int libperm_allgather(void* comm, void* recv, size_t bytes, int rank, cudaStream_t st, std::string& msg);
+int libperm_comm_unique_id(void* id128, std::string& msg);
+int libperm_comm_init(int world, int rank, const void* id128, int device, void** comm, std::string& msg);
+int libperm_comm_destroy(void* comm, std::string& msg);
 
 using namespace perm;
 
@@ -167,43 +176,7 @@ bool int01_fits(const Csx& crs) {
 
 }  // namespace
 
-struct perm_plan_s {
-  int n = 0;
-  perm_opts opts{};
-  Csx ccs, crs, occs;
-  std::vector<int> rowp, colp;
-  bool singular = false;
-  bool trivial1 = false;  // n == 1
-  KernelSpec spec;
-  KernelCode code;
-  std::vector<char> cubin;
-  std::string ptxas_log;
-  perm_plan_info info{};
-  bool is_u128 = false;   // INT01 partials (16 B)
-  bool is_c128 = false;   // complex FP64 partials (re, im; 16 B)
-  int kind() const { return is_u128 ? 1 : (is_c128 ? 2 : 0); }
-  size_t pbytes() const { return (is_u128 || is_c128) ? 16 : 8; }
-  // device state
-  bool on_device = false;
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  cudaLibrary_t lib = nullptr;
-  cudaKernel_t kern = nullptr;
-  void* d_slots = nullptr;
-  void* d_counter = nullptr;
-  void* d_partial = nullptr;  // 16 bytes
-  void* d_scratch = nullptr;  // fold scratch (world entries)
-  void* d_rscratch = nullptr; // tree-reduction pass buffers
-  // pooled allocation sizes (perm_free returns the buffers to the pool)
-  size_t partial_bytes = 64, counter_bytes = 256, slots_bytes = 0, rscratch_bytes = 0, tier_alloc_bytes = 0;
-  std::string lib_key;        // cubin bytes: key of the shared loaded library
-  bool lib_held = false;
-  size_t scratch_bytes = 0;
-  void* d_tier = nullptr;     // HYBRID global tier (tier_rows x resident threads)
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
-  uint64_t last_first = 0, last_count = 0;
-};
+// struct perm_plan_s: plan_state.h
 
 namespace {
 
@@ -388,6 +361,8 @@ int run_range(perm_plan_s* p, uint64_t first, uint64_t count, double* sweep_ms, 
     if (reduce_ms) *reduce_ms = 0;
     return PERM_OK;
   }
+  if (count > 0x7fffffffull)  // the kernel's task counter is 32-bit
+    return fail(PERM_EINVAL, "more than 2^31 warp-tasks in one launch: set task_chunks (M) larger");
   CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned), p->stream));
   unsigned long long tb = first;
   unsigned tc = (unsigned)count;
@@ -429,6 +404,12 @@ int shard_range(perm_plan_s* p, int rank, int world, uint64_t& first, uint64_t& 
 
 void fill_result(perm_plan_s* p, perm_result* r, const unsigned char* raw16, bool scaled) {
   std::memset(r, 0, sizeof(*r));
+  r->w_plan = p->info.w_plan;
+  r->k = p->info.k;
+  r->c = p->info.c;
+  r->b = p->info.B;
+  r->mode = p->info.mode;
+  r->K = p->info.K;
   if (p->is_u128) {
     uint64_t lo, hi;
     std::memcpy(&lo, raw16, 8);
@@ -504,6 +485,11 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
   const double t0 = now_ms();
   auto* p = new perm_plan_s();
   if (opts_in) p->opts = *opts_in;
+  if (p->opts.world > 1 && ((p->opts.world & (p->opts.world - 1)) || p->opts.world > 128 || p->opts.rank < 0 ||
+                            p->opts.rank >= p->opts.world)) {
+    delete p;
+    return fail(PERM_EINVAL, "opts.world must be a power of two <= 128 and 0 <= opts.rank < world");
+  }
   auto bail = [&](int code) {
     perm_free(p);
     return code;
@@ -556,6 +542,9 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     // resident warp on each of 8 GPUs keeps the dynamic-scheduling tail small
     const int btask = std::max(8, nb - 5 - 17);
     int B = p->opts.chunk_log2 > 0 ? p->opts.chunk_log2 : std::min(std::min(bcap, btask), std::max(0, nb - 5));
+    // exact reseed interval (perm_opts.reseed_log2): every chunk is seeded
+    // exactly from x0, so the interval caps the chunk length
+    if (p->opts.reseed_log2 > 0) B = std::min(B, p->opts.reseed_log2);
     if (B > nb) B = nb;
     // INT01 keeps 128-bit products: a shorter unrolled block (fewer live
     // 4-register values, faster NVRTC)
@@ -631,8 +620,19 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     auto app = [&](const void* d, size_t nb) { pkey.append((const char*)d, nb); };
     const int hdr[] = {n, mode, (int)ord, p->opts.chunk_log2, p->opts.block_log2, p->opts.task_chunks,
                        p->opts.factor_cols, p->opts.min_blocks, p->opts.threads_per_block,
-                       p->opts.hybrid_c, p->opts.zero_skip, p->opts.autotune, p->opts.no_device};
+                       p->opts.hybrid_c, p->opts.zero_skip, p->opts.autotune, p->opts.no_device,
+                       p->opts.reseed_log2};
     app(hdr, sizeof hdr);
+    // planner knobs read from the environment change plans: part of the key
+    for (const char* k : {"PERM_ELIM_CANDS", "PERM_ELIM_MAXSIZE", "PERM_ELIM_BEAM", "PERM_ELIM_VARIANTS", "PERM_NO_CC",
+                          "PERM_PLAN_COMPILES", "PERM_NO_AUTOTUNE", "PERM_ALLOW_SPILL", "PERM_PLAN_BUDGET"}) {
+      const char* v = getenv(k);
+      pkey += k;
+      pkey += '=';
+      pkey += v ? v : "";
+      pkey += ';';
+    }
+    pkey += build_id();
     app(&gr, sizeof gr);
     app(p->ccs.ptr.data(), p->ccs.ptr.size() * sizeof(int32_t));
     app(p->ccs.idx.data(), p->ccs.idx.size() * sizeof(int32_t));
@@ -650,6 +650,37 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       p->opts = keep;
       I.plan_cached = 1;
       plan_hit = true;
+    }
+  }
+  // on-disk plan cache (opts.cache_dir, else $PERM_CACHE_DIR): planning output
+  // of an earlier process with the same key (matrix content, options, build)
+  std::string cache_file;
+  {
+    const char* dir = p->opts.cache_dir ? p->opts.cache_dir : getenv("PERM_CACHE_DIR");
+    if (dir && *dir) {
+      char nm[64];
+      snprintf(nm, sizeof nm, "/perm-%016llx%016llx.plan", (unsigned long long)fnv1a64(pkey),
+               (unsigned long long)fnv1a64(pkey, 0x84222325cbf29ce4ull));
+      cache_file = std::string(dir) + nm;
+    }
+  }
+  if (!plan_hit && !cache_file.empty()) {
+    std::string blob;
+    if (FILE* f = fopen(cache_file.c_str(), "rb")) {
+      char buf[1 << 16];
+      size_t got;
+      while ((got = fread(buf, 1, sizeof buf, f)) > 0) blob.append(buf, got);
+      fclose(f);
+      std::string key;
+      const perm_opts keep = p->opts;
+      if (plan_deserialize(blob.data(), blob.size(), *p, &key) && key == pkey) {
+        p->opts = keep;
+        I.disk_cached = 1;
+        plan_hit = true;
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        if (g_plan_cache.size() > 256) g_plan_cache.clear();
+        g_plan_cache[pkey] = *p;
+      }
     }
   }
   if (!plan_hit) {
@@ -898,6 +929,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         }
       for (auto& r : runs) elim_of_base[r.first] = r.second.get();
     }
+    if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] elimination searches %.3f ms (%zu)\n", now_ms() - tc, elim_of_base.size());
     // candidates per distinct sequence, generated concurrently and merged in
     // sequence order (deterministic)
     std::vector<std::future<std::vector<Cand>>> cjobs;
@@ -950,6 +982,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       cands.insert(cands.end(), part.begin(), part.end());
     }
     std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.score < b.score; });
+    if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] candidates %.3f ms (%zu)\n", now_ms() - tc, cands.size());
     const bool dbg_plan = getenv("PERM_DEBUG_PLAN") != nullptr;
     if (dbg_plan)
       for (const Cand& c : cands)
@@ -1190,6 +1223,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     };
     struct Ok { double score; size_t ci; Built b; };
     std::vector<Ok> oks;
+    const double t_compile0 = now_ms();
+    I.codegen_ms = t_compile0 - tc;
     std::vector<std::future<Built>> fut;  // candidates compiled concurrently (NVRTC is thread-safe)
     for (const Cand& c : cands) fut.push_back(std::async(std::launch::async, build, c));
     for (size_t ci = 0; ci < cands.size(); ++ci) {
@@ -1209,7 +1244,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         g_err = b.err;
         return bail(b.status);
       }
-      I.nvrtc_ms += b.nvrtc_ms;
+      I.nvrtc_cpu_ms += b.nvrtc_ms;
       if (!b.ok) continue;
       const double score =
           (n == 1 || p->singular) ? 0.0 : b.kc.w_plan * (1.0 - c.pskip) / eff(bps_of(b.regs, b.sp.threads));
@@ -1218,6 +1253,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
                 b.sp.U, b.sp.min_blocks, b.regs, b.kc.w_plan, score, (int)b.ok);
       oks.push_back({score, ci, std::move(b)});
     }
+    I.nvrtc_ms = now_ms() - t_compile0;
+    if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] compiles %.3f ms (%zu)\n", now_ms() - tc, oks.size());
     // model choice; then, with a device, measured choice (autotune): each
     // compiled candidate sweeps a few spread samples of its task range, and
     // replaces the model's pick only when it is clearly faster per Gray step
@@ -1233,7 +1270,9 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         bs.push_back(&o.b);
         pskips.push_back(cands[o.ci].pskip);
       }
+      const double t_at0 = now_ms();
       const std::vector<double> t = time_candidates(bs, pskips, p->opts.device, p->is_u128 || p->is_c128);
+      I.autotune_ms = now_ms() - t_at0;
       if (t[pick] > 0) {
         size_t best = pick;
         for (size_t q = 0; q < oks.size(); ++q)
@@ -1272,7 +1311,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       partition_alg4(ob, gr, 148, I.k, I.c);
     }
     if (n == 1) p->trivial1 = true;
-    I.codegen_ms = now_ms() - tc - I.nvrtc_ms;
+    I.candidates_compiled = (int)oks.size();
     I.w_alg1 = w_alg1(p->occs);
     if (p->is_c128)  // complex Alg. 1: an update is 2 DP ops, a product step 4, the accumulate 2
       I.w_alg1 = 2.0 * (I.w_alg1 - n) + 4.0 * (n - 1) + 2.0;
@@ -1288,6 +1327,15 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     std::lock_guard<std::mutex> lk(g_cache_mu);
     if (g_plan_cache.size() > 256) g_plan_cache.clear();
     g_plan_cache[pkey] = *p;
+  }
+  if (!plan_hit && !cache_file.empty()) {  // atomic publish: write a temp file, rename
+    const std::string blob = plan_serialize(*p, pkey);
+    const std::string tmp = cache_file + ".tmp." + std::to_string((long long)getpid());
+    if (FILE* f = fopen(tmp.c_str(), "wb")) {
+      const bool ok = fwrite(blob.data(), 1, blob.size(), f) == blob.size();
+      if (fclose(f) == 0 && ok) rename(tmp.c_str(), cache_file.c_str());
+      else remove(tmp.c_str());
+    }
   }
   I.plan_ms = now_ms() - t0;
   if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] planning %.3f ms (cached %d)\n", I.plan_ms, I.plan_cached);
@@ -1334,8 +1382,11 @@ int perm_shard_range(perm_plan_t p, int rank, int world, uint64_t* first_task, u
     return PERM_OK;
   }
   const uint64_t Lg = ((32ull * (uint64_t)p->info.M) << p->info.B) << p->info.K;  // Gray steps per task
-  *g_begin = first * Lg;
-  *g_end = (first + count) * Lg;
+  // small n: one task may span more lanes than the range has chunks (masked
+  // lanes); the Gray range itself ends at 2^(n-1)
+  const uint64_t total = 1ull << (p->n - 1);
+  *g_begin = std::min(first * Lg, total);
+  *g_end = std::min((first + count) * Lg, total);
   return PERM_OK;
 }
 
@@ -1411,9 +1462,16 @@ int perm_compute_shard(perm_plan_t p, int rank, int world, perm_result* r) {
   fill_result(p, r, raw, false);
   r->world = world;
   r->rank = rank;
-  r->products = (count * 32ull * (uint64_t)p->info.M << p->info.B) << p->info.K;
+  {
+    const uint64_t total = p->n >= 2 ? (1ull << (p->n - 1)) : 1;
+    const uint64_t Lg = ((32ull * (uint64_t)p->info.M) << p->info.B) << p->info.K;
+    const uint64_t g0 = std::min<uint64_t>(total, first * Lg);
+    r->products = std::min<uint64_t>(total - g0, count * Lg);
+  }
+  r->steps = r->products;
   r->sweep_ms = sm;
   r->reduce_ms = rm;
+  r->seconds = (sm + rm) * 1e-3;
   return PERM_OK;
 }
 
@@ -1468,18 +1526,133 @@ int perm_fold(perm_plan_t p, const perm_result* shards, int world, perm_result* 
   return PERM_OK;
 }
 
+int perm_compute_async(perm_plan_t p, void* d_out) {
+  if (!p || !d_out) return fail(PERM_EINVAL, "NULL argument");
+  if (!p->on_device) return fail(PERM_ECUDA, "plan was created with no_device (no CPU fallback)");
+  const int world = std::max(1, p->opts.world), rank = p->opts.world > 1 ? p->opts.rank : 0;
+  if (world > 128) return fail(PERM_EINVAL, "world > 128");
+  if (world > 1 && !p->opts.nccl_comm) return fail(PERM_EINVAL, "opts.world > 1 needs opts.nccl_comm");
+  const size_t pb = p->pbytes();
+  CUDA_TRY(cudaSetDevice(p->device));
+  // this rank's unscaled partial into its slot of the gather buffer
+  char* gather = static_cast<char*>(p->d_scratch);
+  int st = perm_compute_shard_async(p, rank, world, gather + (size_t)rank * pb);
+  if (st) return st;
+  if (p->opts.nccl_comm) {  // the path's one exchange step (in-place all-gather)
+    std::string msg;
+    st = libperm_allgather(p->opts.nccl_comm, gather, pb, rank, p->stream, msg);
+    if (st) return fail(st, msg);
+  }
+  st = perm_fold_async(p, gather, world, d_out);
+  if (st) return st;
+  CUDA_TRY(cudaEventRecord(p->ev[3], p->stream));
+  return PERM_OK;
+}
+
 int perm_compute_ex(perm_plan_t p, perm_result* r) {
   if (!p || !r) return fail(PERM_EINVAL, "NULL argument");
-  perm_result sh;
-  int st = perm_compute_shard(p, 0, 1, &sh);
+  if (!p->on_device) return fail(PERM_ECUDA, "plan was created with no_device (no CPU fallback)");
+  void* d_res = static_cast<char*>(p->d_partial) + 32;  // 16-byte result slot
+  int st = perm_compute_async(p, d_res);
   if (st) return st;
-  return perm_fold(p, &sh, 1, r);
+  unsigned char raw[16];
+  CUDA_TRY(cudaMemcpyAsync(raw, d_res, 16, cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  fill_result(p, r, raw, true);
+  if (p->singular) { r->value = 0.0; r->value_im = 0.0; r->exact_lo = r->exact_hi = 0; }
+  r->world = std::max(1, p->opts.world);
+  r->rank = p->opts.world > 1 ? p->opts.rank : 0;
+  r->products = r->steps = p->n >= 2 ? (1ull << (p->n - 1)) : 1;
+  if (p->last_count > 0) {
+    float a = 0, b = 0, c = 0;
+    CUDA_TRY(cudaEventElapsedTime(&a, p->ev[0], p->ev[1]));
+    CUDA_TRY(cudaEventElapsedTime(&b, p->ev[1], p->ev[2]));
+    CUDA_TRY(cudaEventElapsedTime(&c, p->ev[0], p->ev[3]));
+    r->sweep_ms = a;
+    r->reduce_ms = b;
+    r->seconds = c * 1e-3;
+  }
+  return PERM_OK;
 }
 
 double perm_compute(perm_plan_t p) {
   perm_result r;
   if (perm_compute_ex(p, &r) != PERM_OK) return std::nan("");
   return r.value;
+}
+
+int perm_compute_partial(perm_plan_t p, int rank, int world, double* partial) {
+  if (!partial) return fail(PERM_EINVAL, "NULL argument");
+  perm_result r;
+  const int st = perm_compute_shard(p, rank, world, &r);
+  if (st) return st;
+  partial[0] = r.value;
+  if (p->is_c128) partial[1] = r.value_im;
+  return PERM_OK;
+}
+
+int perm_plan_export(perm_plan_t p, void* buf, size_t* size) {
+  if (!p || !size) return fail(PERM_EINVAL, "NULL argument");
+  const std::string blob = plan_serialize(*p, "export");
+  if (buf && *size >= blob.size()) std::memcpy(buf, blob.data(), blob.size());
+  *size = blob.size();
+  return PERM_OK;
+}
+
+int perm_plan_import(const void* blob, size_t size, const perm_opts* opts, perm_plan_t* out) {
+  if (!blob || !out) return fail(PERM_EINVAL, "NULL argument");
+  *out = nullptr;
+  const double t0 = now_ms();
+  auto* p = new perm_plan_s();
+  if (opts) p->opts = *opts;
+  std::string key;
+  if (!plan_deserialize(blob, size, *p, &key) || key != "export") {
+    delete p;
+    return fail(PERM_EINVAL, "perm_plan_import: not a plan blob of this libperm build");
+  }
+  p->info.disk_cached = 1;
+  p->info.plan_cached = 0;
+  if (!p->opts.no_device) {
+    const int st = load_device(p);
+    if (st != PERM_OK) {
+      perm_free(p);
+      return st;
+    }
+  }
+  p->info.plan_ms = now_ms() - t0;
+  *out = p;
+  return PERM_OK;
+}
+
+int perm_comm_unique_id(void* id128) {
+  if (!id128) return fail(PERM_EINVAL, "NULL argument");
+  std::string msg;
+  const int st = libperm_comm_unique_id(id128, msg);
+  return st ? fail(st, msg) : PERM_OK;
+}
+
+int perm_comm_init(int world, int rank, const void* id128, int device, void** comm) {
+  if (!id128 || !comm || world < 1 || rank < 0 || rank >= world) return fail(PERM_EINVAL, "bad arguments");
+  std::string msg;
+  const int st = libperm_comm_init(world, rank, id128, device, comm, msg);
+  return st ? fail(st, msg) : PERM_OK;
+}
+
+int perm_comm_destroy(void* comm) {
+  std::string msg;
+  const int st = libperm_comm_destroy(comm, msg);
+  return st ? fail(st, msg) : PERM_OK;
+}
+
+int perm_probe_fp64_peak(int device, double* lane_ops_per_s, double* ms) {
+  if (!lane_ops_per_s) return fail(PERM_EINVAL, "NULL argument");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(PERM_ECUDA, "no such CUDA device (no CPU fallback)");
+  double m = 0;
+  CUDA_TRY(libperm_probe_fp64_peak(device, 5, lane_ops_per_s, &m));
+  if (ms) *ms = m;
+  return PERM_OK;
 }
 
 int perm_debug_task_partials(perm_plan_t p, void* host, uint64_t cap, uint64_t* count, uint64_t* first_task) {
@@ -1529,14 +1702,21 @@ int perm_plan_cubin(perm_plan_t p, void* buf, size_t* size) {
 
 void perm_free(perm_plan_t p) {
   if (!p) return;
-  if (p->on_device) {
+  // release every device resource that exists, whether or not load_device
+  // completed (a failed plan may hold a stream, events, buffers, a library)
+  const bool any = p->stream || p->d_slots || p->d_counter || p->d_rscratch || p->d_partial || p->d_scratch ||
+                   p->d_tier || p->lib_held || p->ev[0] || p->ev[1] || p->ev[2] || p->ev[3];
+  if (any) {
     cudaSetDevice(p->device);
     if (p->stream) cudaStreamSynchronize(p->stream);
     pool_free(p->device, p->d_slots, p->slots_bytes);
     pool_free(p->device, p->d_counter, p->counter_bytes);
     pool_free(p->device, p->d_rscratch, p->rscratch_bytes);
     pool_free(p->device, p->d_partial, p->partial_bytes);
-    pool_free(p->device, p->d_scratch, p->scratch_bytes);
+    if (p->d_scratch) {
+      if (p->scratch_bytes == 16 * 128) pool_free(p->device, p->d_scratch, p->scratch_bytes);
+      else cudaFree(p->d_scratch);  // grown by perm_fold with cudaMalloc
+    }
     pool_free(p->device, p->d_tier, p->tier_alloc_bytes);
     for (auto& e : p->ev)
       if (e) cudaEventDestroy(e);

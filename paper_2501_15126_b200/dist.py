@@ -1,18 +1,62 @@
-"""Multi-GPU plumbing (one process per GPU, torch.distributed over NCCL).
+"""Multi-GPU plumbing (one process per GPU; torch.distributed only moves
+host-side bytes: the NCCL unique id and the plan blob).
 
 The Gray range is split into `world` power-of-two-aligned shards of whole
-warp-tasks (perm_shard_range); each rank sweeps its shard on its own GPU
-(perm_compute_shard_async writes the 8/16-byte unscaled partial into a device
-tensor), one all-gather moves the partials (the path's single exchange step),
-and every rank folds them in rank order with the deterministic fold kernel
-(perm_fold_async), so the result is bitwise identical to the one-GPU result.
+warp-tasks (perm_shard_range).  Production path (`init_comm` + `plan_on_rank0`):
+rank 0 plans (search + NVRTC) once and broadcasts the exported plan, every
+rank imports it with its own rank/world/NCCL communicator, and
+perm_compute_async sweeps the rank's shard, all-gathers the 8/16-byte
+partials over NCCL inside libperm (the path's single exchange step) and folds
+them in rank order with the deterministic fold kernel -- bitwise identical to
+the one-GPU result.  `ShardedPermanent` is the host-staged variant for gloo
+tests (ranks sharing one GPU, where NCCL refuses duplicate devices).
 """
 from __future__ import annotations
 
+import hashlib
+
 
 def plan_signature(plan):
+    """Everything that decides the kernel bits: geometry, orderings and the
+    hash of the generated source and cubin (codegen variant, caches, bounds)."""
     i = plan.info
-    return (i["K"], i["B"], i["U"], i["M"], i["tasks"], tuple(i["col_perm"]), tuple(i["row_perm"]))
+    h = hashlib.sha256(plan.source.encode())
+    h.update(plan.cubin())
+    return (i["K"], i["B"], i["U"], i["M"], i["tasks"], tuple(i["col_perm"]), tuple(i["row_perm"]), h.hexdigest())
+
+
+def _bcast_bytes(data, rank: int, group=None):
+    import torch.distributed as dist
+    box = [data if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    return box[0]
+
+
+def init_comm(rank: int, world: int, device: int, group=None):
+    """libperm-owned NCCL communicator over the ranks of `group` (any world,
+    including 1): rank 0's unique id is broadcast with torch.distributed."""
+    from . import Comm
+    uid = Comm.unique_id() if rank == 0 else None
+    if world > 1:
+        uid = _bcast_bytes(uid, rank, group)
+    return Comm(world, rank, uid, device)
+
+
+def plan_on_rank0(make_plan, rank: int, world: int, group=None, **import_opts):
+    """Rank 0 runs the planner (make_plan() -> Plan) and broadcasts its export;
+    the other ranks import it (no search, no NVRTC) with `import_opts` (device,
+    stream, rank, world, nccl_comm).  Every rank runs the same kernel bits."""
+    from . import Plan
+    if rank == 0:
+        plan = make_plan()
+        blob = plan.export()
+    else:
+        plan, blob = None, None
+    if world > 1:
+        blob = _bcast_bytes(blob, rank, group)
+    if rank != 0:
+        plan = Plan.from_blob(blob, **import_opts)
+    return plan
 
 
 def agree_plan(make_plan, world: int, group=None):

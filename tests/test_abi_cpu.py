@@ -2,6 +2,7 @@
 symbol include/perm.h declares; host planner entry points match the planner
 oracle bit for bit; codegen + NVRTC (sm_100a) run without a GPU and produce
 spill-free kernels.  No compute call is made (no GPU here)."""
+import json
 import os
 import re
 import shutil
@@ -14,6 +15,7 @@ import pytest
 import paper_2501_15126_b200 as pb
 from paper_2501_15126_b200 import _abi
 from oracle import planner as OP
+from conftest import ROOT
 import synth
 from conftest import ROOT
 
@@ -320,3 +322,72 @@ def test_smem_placement_of_values_the_body_never_touches():
     for nm_ in names:
         assert not re.search(rf"\b{nm_}\b", body) and f"SM_{nm_}" not in body
     assert "extern __shared__" in src
+
+
+# ---- round 2: plan transport (disk cache, rank-0 broadcast), knobs in the key ----
+
+def test_plan_export_import_roundtrip_no_device():
+    A = synth.erdos_renyi(24, 0.3, 2)
+    P = pb.Plan.from_dense(A, mode="reg", no_device=True, autotune=-1)
+    blob = P.export()
+    Q = pb.Plan.from_blob(blob, no_device=True)
+    assert Q.source == P.source and Q.cubin() == P.cubin()
+    a, b = P.info, Q.info
+    for k in ("n", "nnz", "K", "B", "U", "M", "tasks", "w_plan", "row_perm", "col_perm", "mode"):
+        assert a[k] == b[k], k
+    assert b["disk_cached"] == 1
+    with pytest.raises(pb.PermError):
+        pb.Plan.from_blob(blob[:-7], no_device=True)          # truncated
+    with pytest.raises(pb.PermError):
+        pb.Plan.from_blob(b"X" + blob[1:], no_device=True)    # foreign magic
+
+
+def test_disk_plan_cache(tmp_path):
+    A = synth.erdos_renyi(22, 0.3, 5)
+    d = str(tmp_path)
+    P = pb.Plan.from_dense(A, mode="reg", no_device=True, autotune=-1, cache_dir=d)
+    assert P.info["disk_cached"] == 0
+    files = os.listdir(d)
+    assert len(files) == 1 and files[0].endswith(".plan")
+    # a new process would miss the in-process cache; a different option set is a
+    # different key (the in-process cache is keyed identically, so force the disk
+    # path by planning through a fresh library state: load the blob directly)
+    Q = pb.Plan.from_dense(A, mode="reg", no_device=True, autotune=-1, cache_dir=d)
+    assert Q.source == P.source
+    R = pb.Plan.from_dense(A * 0.5, mode="reg", no_device=True, autotune=-1, cache_dir=d)
+    assert len(os.listdir(d)) == 2 and R.source != P.source
+
+
+def test_disk_plan_cache_in_fresh_process(tmp_path):
+    """A second process plans the same matrix from the disk cache: no search,
+    no NVRTC, identical kernel."""
+    import subprocess
+    import sys
+    code = ("import sys, json; sys.path.insert(0, %r); import synth, paper_2501_15126_b200 as pb; "
+            "P = pb.Plan.from_dense(synth.erdos_renyi(26, 0.25, 3), mode='reg', no_device=True, autotune=-1, "
+            "cache_dir=%r); i = P.info; print(json.dumps([i['disk_cached'], i['plan_ms'], len(P.source)]))"
+            % (ROOT, str(tmp_path)))
+    out1 = json.loads(subprocess.check_output([sys.executable, "-c", code]).decode().strip().splitlines()[-1])
+    out2 = json.loads(subprocess.check_output([sys.executable, "-c", code]).decode().strip().splitlines()[-1])
+    assert out1[0] == 0 and out2[0] == 1 and out1[2] == out2[2]
+    assert out2[1] < 0.5 * out1[1]
+
+
+def test_env_knobs_are_part_of_the_plan_key(monkeypatch):
+    A = synth.erdos_renyi(20, 0.3, 8)
+    P = pb.Plan.from_dense(A, mode="reg", no_device=True, autotune=-1)
+    monkeypatch.setenv("PERM_NO_CC", "1")
+    Q = pb.Plan.from_dense(A, mode="reg", no_device=True, autotune=-1)
+    assert Q.info["plan_cached"] == 0
+
+
+def test_opts_world_validation_and_result_fields():
+    A = synth.erdos_renyi(12, 0.4, 1)
+    with pytest.raises(pb.PermError):
+        pb.Plan.from_dense(A, no_device=True, world=3, rank=0)
+    with pytest.raises(pb.PermError):
+        pb.Plan.from_dense(A, no_device=True, world=4, rank=4)
+    P = pb.Plan.from_dense(A, no_device=True, reseed_log2=4)
+    assert P.info["B"] <= 4
+    with pytest.raises(pb.PermError):   # no device: compute fails loudly (no CPU fallback)
+        P.compute_ex()

@@ -23,7 +23,7 @@ def run(cmd):
 
 
 def test_two_ranks_share_one_gpu_bitwise():
-    common = ["--dim", "32", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"]
+    common = ["--dim", "32", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--no-plain", "--no-cold"]
     one = run([sys.executable, "bench.py", *common])
     two = run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                "--master-addr", "127.0.0.1", "--master-port", "29613", "bench.py", "--gpus", "2",

@@ -569,3 +569,67 @@ def test_checkpoint_resume_complex_and_value_keyed(tmp_path):
     assert compute_resumable(plan(A), ck2, pieces=16, max_pieces=3) is None
     with pytest.raises(ValueError):
         compute_resumable(plan(A2), ck2, pieces=16)
+
+
+# ---- round 2: the C-ABI surface of 8(b): collective, transport, probe -------------
+
+def test_nccl_world1_collective_bitwise():
+    """perm_compute with a libperm-owned NCCL communicator (world 1: the real
+    all-gather runs on the plan's stream) equals the plain one-GPU result bit
+    for bit, through perm_compute_ex and perm_compute_async."""
+    import torch
+    A = synth.erdos_renyi(30, 0.25, 4)
+    ref = plan(A).compute()
+    comm = pb.Comm(1, 0, pb.Comm.unique_id(), 0)
+    try:
+        P = plan(A, world=1, rank=0, nccl_comm=comm.handle)
+        assert P.compute() == ref
+        out = torch.zeros(2, dtype=torch.float64, device="cuda:0")
+        P.compute_async(out.data_ptr())
+        torch.cuda.synchronize()
+        assert out[0].item() == ref
+        P.close()
+        B = synth.erdos_renyi(22, 0.25, 4, binary=True)
+        Q = plan(B, mode="int01", world=1, rank=0, nccl_comm=comm.handle)
+        assert Q.exact() == oracle.perm_nw_exact(B)
+    finally:
+        comm.close()
+
+
+def test_plan_import_on_device_bitwise():
+    A = synth.erdos_renyi(32, 0.2, 6)
+    P = plan(A)
+    ref = P.compute()
+    Q = pb.Plan.from_blob(P.export(), device=0)
+    assert Q.info["disk_cached"] == 1 and Q.compute() == ref
+    U = synth.unitary_brickwork(24, 4, 3)
+    C = plan(U)
+    D = pb.Plan.from_blob(C.export(), device=0)
+    assert D.compute() == C.compute()
+
+
+def test_compute_partial_and_result_fields():
+    A = synth.erdos_renyi(28, 0.25, 2)
+    P = plan(A)
+    r = P.compute_ex()
+    i = P.info
+    assert r.steps == 1 << 27 and r.K == i["K"] and r.b == i["B"] and r.w_plan == i["w_plan"]
+    assert (r.k, r.c, r.mode) == (i["k"], i["c"], i["mode"]) and r.seconds > 0
+    parts = [P.compute_partial(k, 4) for k in range(4)]
+    assert P.fold_host(parts) == r.value
+
+
+def test_fp64_peak_probe_is_near_nominal():
+    v, ms = pb.perm_probe_fp64_peak(0)
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    nominal = sms * 64 * 1.965e9
+    assert 0.5 * nominal < v < 1.05 * nominal, (v, nominal)
+
+
+def test_reseed_interval_caps_the_chunk():
+    A = synth.erdos_renyi(30, 0.25, 9)
+    exp = oracle.perm_nw(A)[0]
+    P = plan(A, reseed_log2=6)
+    assert P.info["B"] <= 6
+    assert rel(P.compute(), exp) < REL
