@@ -421,7 +421,7 @@ def main():
         comm = init_comm(rank, world, local)
         dkw = dict(rank=rank, world=world, nccl_comm=comm.handle)
         plan = plan_on_rank0(lambda: pb.Plan(n, pb.PERM_CCS, ptr, idx, val, args.ordering, **kw, **dkw),
-                             rank, world, device=local, stream=stream.cuda_stream, **dkw)
+                             device=local, stream=stream.cuda_stream, **dkw)
         out = torch.zeros(2, dtype=torch.float64, device=dev)
         collective = f"NCCL all-gather of {8 if plan.partial_bytes == 8 else 16} B per rank inside libperm " \
                      f"(perm_compute_async; libperm-owned communicator of {world} rank(s))"

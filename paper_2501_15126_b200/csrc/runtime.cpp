@@ -4,6 +4,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -847,10 +848,16 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     // 2: U <= 3.  ev / 3: greedy or beam search.  The W landscape is rugged (a
     // greedy path can end far from the best, and a beam is not a superset of
     // the greedy path), so the sequences of every search become candidates.
-    auto greedy_elim = [&](const std::vector<int>& rp, const std::vector<int>& cp, int ev) {
+    // W of a partial elimination sequence depends on (base ordering, scoring,
+    // sequence) only -- not on the search kind or the composite bound -- so
+    // the 18 searches per base share one memo (each sequence is generated once)
+    std::mutex memo_mu;
+    std::map<std::pair<int, std::vector<int>>, std::shared_future<double>> memo;
+    std::atomic<int> memo_evals{0}, memo_hits{0};
+    auto greedy_elim = [&](int base, const std::vector<int>& rp, const std::vector<int>& cp, int ev) {
       std::vector<int> seq;
       if (kcap == 0) return seq;
-      auto evalW = [&, ev](const std::vector<int>& s) {
+      auto evalW_raw = [&, ev](const std::vector<int>& s) {
         const int k = (int)s.size();
         std::vector<int> c = costsort_swept(p->ccs, factored_columns(cp, s, k), k);
         Csx o = permute_ccs(p->ccs, rp, c);
@@ -867,6 +874,31 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
           sp.hybrid_c = std::max(std::min(c4 - k, sp.B), std::min(sp.U, sp.B));
         }
         return generate_kernel(o, make_x0(o), sp).w_plan;
+      };
+      auto evalW = [&, base, ev](const std::vector<int>& s) {
+        const std::pair<int, std::vector<int>> key{base * 4 + ev % 3, s};
+        std::promise<double> pr;
+        std::shared_future<double> f;
+        bool owner = false;
+        {
+          std::lock_guard<std::mutex> lk(memo_mu);
+          auto it = memo.find(key);
+          if (it != memo.end()) {
+            f = it->second;
+          } else {
+            f = pr.get_future().share();
+            memo.emplace(key, f);
+            owner = true;
+          }
+        }
+        if (!owner) {
+          ++memo_hits;
+          return f.get();
+        }
+        ++memo_evals;
+        const double v = evalW_raw(s);
+        pr.set_value(v);
+        return v;
       };
       // beam search (width 1 = greedy) over elimination sequences
       std::vector<std::pair<double, std::vector<int>>> beam = {{evalW(seq), seq}};
@@ -924,12 +956,14 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
           runs.emplace_back(base * 32 + ev, std::async(std::launch::async, [&, base, ev] {
                               std::vector<int> rp, cp;
                               order_with(base, rp, cp);
-                              return greedy_elim(rp, cp, ev);
+                              return greedy_elim(base, rp, cp, ev);
                             }));
         }
       for (auto& r : runs) elim_of_base[r.first] = r.second.get();
     }
-    if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] elimination searches %.3f ms (%zu)\n", now_ms() - tc, elim_of_base.size());
+    if (getenv("PERM_DEBUG_TIMING"))
+      fprintf(stderr, "[timing] elimination searches %.3f ms (%zu; %d evaluations, %d memo hits)\n", now_ms() - tc,
+              elim_of_base.size(), memo_evals.load(), memo_hits.load());
     // candidates per distinct sequence, generated concurrently and merged in
     // sequence order (deterministic)
     std::vector<std::future<std::vector<Cand>>> cjobs;
@@ -945,8 +979,13 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       std::vector<int> rp, cp;
       order_with(base, rp, cp);
       const int kmax = (int)picks.size();
-      const int kmin = p->opts.factor_cols > 0 ? kmax : (ev == 0 ? 0 : std::max(0, kmax - 2));
-      for (int K = kmin; K <= kmax; ++K)
+      const int kmin = p->opts.factor_cols > 0 ? kmax : std::max(0, kmax - 2);
+      // K in [kmax-2, kmax], plus the plain sweep K = 0 from the first search
+      // (intermediate K never ranks near the top: W falls steeply with K)
+      std::vector<int> Ks;
+      if (ev == 0 && kmin > 0) Ks.push_back(0);
+      for (int K = kmin; K <= kmax; ++K) Ks.push_back(K);
+      for (int K : Ks)
         for (int var = 0; var < nvar + (mode == PERM_MODE_INT01 && p->opts.zero_skip >= 0 ? 2 : 0); ++var) {
           const int vv = var < nvar ? var : 2 + (var - nvar);
           Csx o = permute_ccs(p->ccs, rp, colp_of(cp, picks, K, vv));
@@ -1183,42 +1222,100 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       b.sp.cc = c.cc;
       set_hybrid(b.sp, b.o);
       if (n == 1 || p->singular) { b.ok = true; return b; }
-      int stack = 0, spill = 0;
       // start at <= 255 registers (2 blocks/SM: the FP64 pipe is already ~95 %
       // busy there); 3 blocks only for clearly small kernels
-      b.sp.min_blocks = p->opts.min_blocks > 0
-                            ? p->opts.min_blocks
-                            : std::min(2, bps_of(generate_kernel(b.o, b.xo, b.sp).est_regs + 16, b.sp.threads));
-      if (p->opts.min_blocks <= 0 && generate_kernel(b.o, b.xo, b.sp).est_regs + 16 <= 152) b.sp.min_blocks = 3;
-      for (int attempt = 0; attempt < 24; ++attempt) {
-        b.kc = generate_kernel(b.o, b.xo, b.sp);
+      {
+        const int est = generate_kernel(b.o, b.xo, b.sp).est_regs;
+        b.sp.min_blocks = p->opts.min_blocks > 0 ? p->opts.min_blocks : std::min(2, bps_of(est + 16, b.sp.threads));
+        if (p->opts.min_blocks <= 0 && est + 16 <= 152) b.sp.min_blocks = 3;
+      }
+      // escalation ladder on a spill: a larger register cap (only steps that
+      // really raise the __launch_bounds__ cap), then a shorter unrolled block,
+      // then fewer chunk bits
+      auto reg_cap = [](int mb, int threads) { return std::min(255, 65536 / (threads * std::max(mb, 1)) / 8 * 8); };
+      auto escalate = [&](KernelSpec& sp, uint64_t& tasks) -> bool {
+        const int cap0 = reg_cap(sp.min_blocks, sp.threads);
+        while (sp.min_blocks > 1) {
+          --sp.min_blocks;
+          if (reg_cap(sp.min_blocks, sp.threads) > cap0) return true;
+        }
+        if (sp.U > 2) { --sp.U; return true; }
+        if (sp.B > 2 && p->opts.chunk_log2 == 0) {
+          const int keepU = sp.U;  // geometry() keeps min_blocks
+          tasks = geometry(c.K, sp, sp.B - 2);
+          set_hybrid(sp, b.o);
+          sp.U = std::min(keepU, sp.B);
+          return true;
+        }
+        return false;
+      };
+      struct Att {
+        KernelSpec sp;
+        uint64_t tasks = 0;
+        KernelCode kc;
+        std::vector<char> cubin;
+        std::string log, err;
+        int status = PERM_OK, regs = -1, stack = 0, spill = 0;
         double ms = 0;
-        b.status = nvrtc_compile(b.kc.source, b.cubin, b.log, p->is_u128, b.cached, ms);
-        if (b.status != PERM_OK) { b.err = g_err; return b; }
-        b.nvrtc_ms += ms;
-        parse_ptxas(b.log, b.regs, stack, spill);
-        {  // authoritative: the cubin's own attributes (the log may be empty, see cubin_attrs)
-          int cr = -1, cf = -1;
-          if (cubin_attrs(b.cubin, cr, cf)) {
-            b.regs = cr;
-            stack = std::max(stack, cf);
-            if (cf > 0) spill = std::max(spill, cf);
-          }
+        bool cached = false;
+      };
+      auto attempt = [&](const KernelSpec& sp, uint64_t tasks) {
+        Att t;
+        t.sp = sp;
+        t.tasks = tasks;
+        t.kc = generate_kernel(b.o, b.xo, sp);
+        t.status = nvrtc_compile(t.kc.source, t.cubin, t.log, p->is_u128, t.cached, t.ms);
+        if (t.status != PERM_OK) { t.err = g_err; return t; }
+        parse_ptxas(t.log, t.regs, t.stack, t.spill);
+        int cr = -1, cf = -1;  // authoritative: the cubin's own attributes (the log may be empty, see cubin_attrs)
+        if (cubin_attrs(t.cubin, cr, cf)) {
+          t.regs = cr;
+          t.stack = std::max(t.stack, cf);
+          if (cf > 0) t.spill = std::max(t.spill, cf);
         }
         if (getenv("PERM_DEBUG_PLAN"))
-          fprintf(stderr, "[plan]   attempt K %d B %d U %d minb %d cc %d: regs %d stack %d spill %d\n", c.K, b.sp.B,
-                  b.sp.U, b.sp.min_blocks, (int)b.sp.cc, b.regs, stack, spill);
-        if ((stack <= 0 && spill <= 0) || getenv("PERM_ALLOW_SPILL")) { b.ok = true; break; }  // knob: experiments only
-        // escalate: larger register cap, then a shorter unrolled block, then fewer chunk bits
-        if (b.sp.min_blocks > 1) b.sp.min_blocks -= 1;
-        else if (b.sp.U > 2) b.sp.U -= 1;
-        else if (b.sp.B > 2 && p->opts.chunk_log2 == 0) {
-          const int keepU = b.sp.U;  // geometry() keeps min_blocks
-          b.tasks = geometry(c.K, b.sp, b.sp.B - 2);
-          set_hybrid(b.sp, b.o);
-          b.sp.U = std::min(keepU, b.sp.B);
-        } else break;
+          fprintf(stderr, "[plan]   attempt K %d B %d U %d minb %d cc %d: regs %d stack %d spill %d\n", c.K, sp.B, sp.U,
+                  sp.min_blocks, (int)sp.cc, t.regs, t.stack, t.spill);
+        return t;
+      };
+      auto take = [&](Att& t) {
+        b.sp = t.sp;
+        b.tasks = t.tasks;
+        b.kc = std::move(t.kc);
+        b.cubin = std::move(t.cubin);
+        b.log = std::move(t.log);
+        b.regs = t.regs;
+        b.cached = t.cached;
+      };
+      auto clean = [](const Att& t) { return (t.stack <= 0 && t.spill <= 0) || getenv("PERM_ALLOW_SPILL"); };
+      // the first three rungs compile concurrently (speculatively); the first
+      // spill-free rung in ladder order wins -- the same choice as compiling
+      // them one after another, in one compile latency instead of three
+      std::vector<std::pair<KernelSpec, uint64_t>> ladder = {{b.sp, b.tasks}};
+      while (ladder.size() < 3) {
+        auto nx = ladder.back();
+        if (!escalate(nx.first, nx.second)) break;
+        ladder.push_back(nx);
       }
+      std::vector<std::future<Att>> fa;
+      for (auto& rung : ladder) fa.push_back(std::async(std::launch::async, attempt, rung.first, rung.second));
+      std::vector<Att> done;
+      for (auto& f : fa) done.push_back(f.get());
+      for (Att& t : done) {
+        b.nvrtc_ms += t.ms;
+        if (t.status != PERM_OK) { b.status = t.status; b.err = t.err; return b; }
+      }
+      for (Att& t : done)
+        if (clean(t)) { take(t); b.ok = true; return b; }
+      KernelSpec sp = ladder.back().first;
+      uint64_t tasks = ladder.back().second;
+      for (int more = 0; more < 24 && escalate(sp, tasks); ++more) {
+        Att t = attempt(sp, tasks);
+        b.nvrtc_ms += t.ms;
+        if (t.status != PERM_OK) { b.status = t.status; b.err = t.err; return b; }
+        if (clean(t)) { take(t); b.ok = true; return b; }
+      }
+      take(done.back());  // every rung spilled: b.ok stays false
       return b;
     };
     struct Ok { double score; size_t ci; Built b; };

@@ -42,11 +42,12 @@ def init_comm(rank: int, world: int, device: int, group=None):
     return Comm(world, rank, uid, device)
 
 
-def plan_on_rank0(make_plan, rank: int, world: int, group=None, **import_opts):
+def plan_on_rank0(make_plan, group=None, **import_opts):
     """Rank 0 runs the planner (make_plan() -> Plan) and broadcasts its export;
     the other ranks import it (no search, no NVRTC) with `import_opts` (device,
     stream, rank, world, nccl_comm).  Every rank runs the same kernel bits."""
     from . import Plan
+    rank, world = import_opts.get("rank", 0), max(1, import_opts.get("world", 1))
     if rank == 0:
         plan = make_plan()
         blob = plan.export()

@@ -3,6 +3,6 @@
 TAG=${1:-r2}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo smoke rc=$?
-timeout 2400 python -m pytest tests -m gpu -q -x --durations=15 > gpurun_out/${TAG}_gpu_tests.log 2>&1; echo tests rc=$?
+timeout 2400 python -m pytest tests -m gpu -q --durations=25 > gpurun_out/${TAG}_gpu_tests.log 2>&1; echo tests rc=$?
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.log 2>&1; echo bench rc=$?
 tail -5 gpurun_out/${TAG}_gpu_tests.log; tail -1 gpurun_out/${TAG}_bench.log | cut -c1-600
