@@ -495,6 +495,19 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     perm_free(p);
     return code;
   };
+  // the CUDA context is created on a helper thread while the host planner
+  // runs (a cold process spends ~0.3 s in context creation); load_device and
+  // the autotune wait for it
+  std::shared_future<void> ctx_ready;
+  if (!p->opts.no_device) {
+    const int dev = p->opts.device;
+    ctx_ready = std::async(std::launch::async, [dev] {
+                  int nd = 0;
+                  if (cudaGetDeviceCount(&nd) == cudaSuccess && dev >= 0 && dev < nd && cudaSetDevice(dev) == cudaSuccess)
+                    cudaFree(nullptr);
+                  cudaGetLastError();
+                }).share();
+  }
   std::string err;
   int st = complex_input ? validate_and_convert_c(n, fmt, ptr, idx, val, p->ccs, p->crs, err)
                          : validate_and_convert(n, fmt, ptr, idx, val, p->ccs, p->crs, err);
@@ -1274,8 +1287,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
           if (cf > 0) t.spill = std::max(t.spill, cf);
         }
         if (getenv("PERM_DEBUG_PLAN"))
-          fprintf(stderr, "[plan]   attempt K %d B %d U %d minb %d cc %d: regs %d stack %d spill %d\n", c.K, sp.B, sp.U,
-                  sp.min_blocks, (int)sp.cc, t.regs, t.stack, t.spill);
+          fprintf(stderr, "[plan]   attempt K %d B %d U %d minb %d cc %d: regs %d stack %d spill %d w %.5f\n", c.K, sp.B,
+                  sp.U, sp.min_blocks, (int)sp.cc, t.regs, t.stack, t.spill, t.kc.w_plan);
         return t;
       };
       auto take = [&](Att& t) {
@@ -1288,11 +1301,11 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         b.cached = t.cached;
       };
       auto clean = [](const Att& t) { return (t.stack <= 0 && t.spill <= 0) || getenv("PERM_ALLOW_SPILL"); };
-      // the first three rungs compile concurrently (speculatively); the first
+      // the first four rungs compile concurrently (speculatively); the first
       // spill-free rung in ladder order wins -- the same choice as compiling
-      // them one after another, in one compile latency instead of three
+      // them one after another, in one compile latency instead of four
       std::vector<std::pair<KernelSpec, uint64_t>> ladder = {{b.sp, b.tasks}};
-      while (ladder.size() < 3) {
+      while (ladder.size() < 4) {
         auto nx = ladder.back();
         if (!escalate(nx.first, nx.second)) break;
         ladder.push_back(nx);
@@ -1367,6 +1380,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         bs.push_back(&o.b);
         pskips.push_back(cands[o.ci].pskip);
       }
+      if (ctx_ready.valid()) ctx_ready.wait();
       const double t_at0 = now_ms();
       const std::vector<double> t = time_candidates(bs, pskips, p->opts.device, p->is_u128 || p->is_c128);
       I.autotune_ms = now_ms() - t_at0;
@@ -1437,6 +1451,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
   I.plan_ms = now_ms() - t0;
   if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] planning %.3f ms (cached %d)\n", I.plan_ms, I.plan_cached);
   if (!p->opts.no_device) {
+    if (ctx_ready.valid()) ctx_ready.wait();
     st = load_device(p);
     if (st != PERM_OK) return bail(st);
   }
