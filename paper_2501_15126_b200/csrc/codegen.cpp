@@ -214,7 +214,36 @@ struct Gen {
         for (int r : fac[f].rows) {
           tier_slot[r] = slots++;
           tier_of[xv(r)] = tier_slot[r];
+          tier_row.push_back(r);
         }
+  }
+  // HYBRID tier vectorisation: slots 2p and 2p+1 of a thread are adjacent
+  // (double2 / int2 per thread, coalesced across the warp: one 16-byte or
+  // 8-byte access moves a row pair); complex rows are 16 bytes already
+  std::vector<int> tier_row;             // slot -> row
+  bool tier_pairs() const { return !cx; }
+  int tier_partner(int r) const {
+    if (!tier_pairs() || tier_slot[r] < 0) return -1;
+    const int q = tier_slot[r] ^ 1;
+    return q < (int)tier_row.size() ? tier_row[q] : -1;
+  }
+  const char* VT2() const { return i01 ? "int2" : "double2"; }
+  // store the tier rows in `rows` (value ids from `val`), pairing partners
+  void tier_store(const std::vector<int>& rows, const std::function<int(int)>& val) {
+    std::set<int> done;
+    for (int r : rows) {
+      if (done.count(r)) continue;
+      const int q = tier_partner(r);
+      if (q >= 0 && std::find(rows.begin(), rows.end(), q) != rows.end()) {
+        const int lo = tier_slot[r] < tier_slot[q] ? r : q, hi = lo == r ? q : r;
+        line(std::string("TIER2(") + std::to_string(tier_slot[lo] >> 1) + ") = make_" + VT2() + "(" + nm(val(lo)) +
+             ", " + nm(val(hi)) + ");");
+        done.insert(q);
+      } else {
+        line("TIER(" + std::to_string(tier_slot[r]) + ") = " + nm(val(r)) + ";");
+      }
+      done.insert(r);
+    }
   }
   bool has_tier() const { return !tier_levels.empty(); }
   bool tierf(int f) const { return fac[f].level >= cT; }
@@ -481,16 +510,18 @@ struct Gen {
   }
 
   void end_region() {  // write loop-carried registers (and tier rows) back
+    std::vector<int> tier_dirty;
     for (const std::string& r : dirty) {
       const int id = cur[r];
       auto t = tier_of.find(r);
       if (t != tier_of.end()) {
-        line("TIER(" + std::to_string(t->second) + ") = " + nm(id) + ";");
+        tier_dirty.push_back(tier_row[t->second]);
         continue;
       }
       if (vals[id].op == 'L' && vals[id].name == r) continue;
       line(r + " = " + nm(id) + ";");
     }
+    tier_store(tier_dirty, [&](int row) { return cur[xv(row)]; });
     dirty.clear();
   }
 
@@ -499,6 +530,19 @@ struct Gen {
     if (tier_slot[r] < 0) return reg(xv(r), xty());
     auto it = cur.find(xv(r));
     if (it != cur.end()) return it->second;
+    const int q = tier_partner(r);
+    if (q >= 0 && !cur.count(xv(q))) {  // one vector load for the row pair
+      const int lo = tier_slot[r] < tier_slot[q] ? r : q, hi = lo == r ? q : r;
+      const std::string v = "tv" + std::to_string(tmp++);
+      line(std::string("const ") + VT2() + " " + v + " = TIER2(" + std::to_string(tier_slot[lo] >> 1) + ");");
+      for (int k = 0; k < 2; ++k) {
+        const std::string name = "t" + std::to_string(tmp++);
+        line(std::string("const ") + VT() + " " + name + " = " + v + (k ? ".y;" : ".x;"));
+        vals.push_back({'M', -1, -1, -1, xty(), name});
+        cur[xv(k ? hi : lo)] = (int)vals.size() - 1;
+      }
+      return cur[xv(r)];
+    }
     std::string name = "t" + std::to_string(tmp++);  // tier load (coalesced across lanes)
     line(std::string("const ") + VT() + " " + name + " = TIER(" + std::to_string(tier_slot[r]) + ");");
     vals.push_back({'M', -1, -1, -1, xty(), name});
@@ -888,11 +932,13 @@ struct Gen {
     for (auto it = nonempty.rbegin(); it != nonempty.rend(); ++it)
       if (*it >= 1 && sreg(*it)) cur["S" + std::to_string(*it)] = mul(qval(*it), above(*it));
     // declare the loop-carried registers
+    std::vector<int> seed_tier;
     for (int r = 0; r < n; ++r) {
       if (dead_row(r) || fac[fac_of_row[r]].level < 0) continue;
-      if (tier_slot[r] >= 0) line("TIER(" + std::to_string(tier_slot[r]) + ") = " + nm(cur[xv(r)]) + ";");
+      if (tier_slot[r] >= 0) seed_tier.push_back(r);
       else line(std::string(VT()) + " " + xv(r) + " = " + nm(cur[xv(r)]) + ";");
     }
+    tier_store(seed_tier, [&](int row) { return cur[xv(row)]; });
     for (int f = 0; f < (int)fac.size(); ++f)
       if (fac[f].group && !fac[f].constant() && fac[f].level >= 0 && !tierf(f) && !zs0(f)) {
         line(rty(dv(f)) + " " + dv(f) + " = " + nm(cur[dv(f)]) + ";");
@@ -1131,8 +1177,9 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
       if (l.alive && l.region == body_region) in_body.insert(l.toks.begin(), l.toks.end());
     struct Mv { int id, size; std::string ty; };
     std::vector<Mv> mv;
+    const bool all = getenv("PERM_SMEM_ALL") != nullptr;
     for (const Ln& l : L)
-      if (l.alive && l.kind == 2 && !in_body.count(l.name)) {
+      if (l.alive && l.kind == 2 && (all || !in_body.count(l.name)) && idname[l.name] != "cacc") {
         const std::string& ty = idname[l.toks[0]];
         mv.push_back({l.name, ty == "int" ? 4 : ((ty == "double" || ty == "i64") ? 8 : 16), ty});
       }
@@ -1260,9 +1307,15 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
          "__device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx c) {\n"
          "  return cplx{fma(a.re, b.re, fma(-a.im, b.im, c.re)), fma(a.re, b.im, fma(a.im, b.re, c.im))}; }\n";
   if (g.i01) o << "typedef unsigned __int128 u128;\ntypedef __int128 i128;\ntypedef long long i64;\n";
-  // HYBRID tier: row slot s of this thread at tier[s * (all threads) + thread]
-  // (the paper's coalesced x[nthreads * row + tid] layout, Listing 4)
-  o << "#define TIER(s) tier[(size_t)(s) * nt_ + gt_]\n";
+  // HYBRID tier: the paper's coalesced x[nthreads * row + tid] layout (Listing 4,
+  // P:543-550), vectorised: row slots 2p, 2p+1 of a thread form one double2
+  // (int2) at pair index p * (all threads) + thread; complex rows: one cplx each
+  if (g.tier_pairs()) {
+    o << "#define TIER(s) tier[((((size_t)((s) >> 1)) * nt_ + gt_) << 1) | ((s) & 1)]\n";
+    o << "#define TIER2(p) (reinterpret_cast<" << g.VT2() << "*>(tier)[(size_t)(p) * nt_ + gt_])\n";
+  } else {
+    o << "#define TIER(s) tier[(size_t)(s) * nt_ + gt_]\n";
+  }
   o << "extern \"C\" __global__ void __launch_bounds__(" << S.threads << ", " << S.min_blocks << ")\n"
     << kc.name << "(const u64 task_begin, const unsigned task_count, const u64 task_stride, "
     << "unsigned* __restrict__ counter, "
@@ -1409,7 +1462,7 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
   int tier_rows = 0;
   for (int r = 0; r < A.n; ++r) tier_rows += g.tier_slot[r] >= 0;
   kc.tier_rows = tier_rows;
-  kc.tier_bytes = tier_rows * (g.i01 ? 4 : (g.cx ? 16 : 8));
+  kc.tier_bytes = (g.tier_pairs() ? (tier_rows + 1) / 2 * 2 : tier_rows) * (g.i01 ? 4 : (g.cx ? 16 : 8));
   kc.live_rows = live - tier_rows;
   kc.levels = (int)g.nonempty.size();
   int qs = 0, ds = 0;

@@ -172,7 +172,9 @@ def test_hybrid_codegen_uses_coalesced_tier():
     i = P.info
     assert i["mode"] == 2 and i["tier_rows"] > 0 and i["local_bytes"] == 0
     src = P.source
-    assert "#define TIER(s) tier[(size_t)(s) * nt_ + gt_]" in src   # x[nthreads*row + tid], Listing 4
+    # x[nthreads*row + tid] (Listing 4), vectorised: row pairs as one double2 per thread
+    assert "#define TIER2(p) (reinterpret_cast<double2*>(tier)[(size_t)(p) * nt_ + gt_])" in src
+    assert "= TIER2(" in src and "TIER2(0) = make_double2(" in src
     assert "SG" in src                                              # cached tier product (globalProduct)
     # same geometry and ordering: the tier takes rows out of the register file
     geo = dict(factor_cols=-1, chunk_log2=i["B"], block_log2=i["U"], ordering=["none", "degree", "permanent"][i["ordering"]])
@@ -180,6 +182,13 @@ def test_hybrid_codegen_uses_coalesced_tier():
     R = pb.Plan.from_dense(A, mode="reg", no_device=True, **geo)
     assert H.info["tier_rows"] > 0 and H.info["reg_rows"] < R.info["reg_rows"]
     assert H.info["regs_per_thread"] <= R.info["regs_per_thread"]
+    # the row pairs move as 128-bit global accesses (LDG.E.128 / STG.E.128)
+    if shutil.which("cuobjdump"):
+        with tempfile.NamedTemporaryFile(suffix=".cubin") as f:
+            f.write(P.cubin())
+            f.flush()
+            sass = subprocess.run(["cuobjdump", "-sass", f.name], capture_output=True, text=True).stdout
+        assert "LDG.E.128" in sass and "STG.E.128" in sass
 
 
 def test_codegen_literals_are_exact_hex():

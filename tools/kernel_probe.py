@@ -26,6 +26,8 @@ WORKLOADS = {
     "complex_band44": (lambda: synth.unitary_brickwork(44, 4, 1), dict()),
     "plain_n40": (lambda: synth.erdos_renyi(40, 0.2, 1), dict(mode="reg", factor_cols=-1)),
     "plain_n36_hybrid": (lambda: synth.erdos_renyi(36, 0.2, 1), dict(mode="hybrid", factor_cols=-1)),
+    "plain_n40_hybrid": (lambda: synth.erdos_renyi(40, 0.2, 1), dict(mode="hybrid", factor_cols=-1)),
+    "plain_n36": (lambda: synth.erdos_renyi(36, 0.2, 1), dict(mode="reg", factor_cols=-1)),
     "bench_n40": (lambda: synth.erdos_renyi(40, 0.2, 1), dict(mode="reg")),
     "band44": (lambda: synth.givens_brickwork(44, 4, 1), dict(mode="reg")),
 }
