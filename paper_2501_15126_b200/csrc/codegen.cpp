@@ -984,6 +984,7 @@ struct PostStats {
   int fused = 0, removed = 0;
   int smem_bytes = 0;  // per block: loop-carried values moved to shared memory
   int moved = 0;
+  int hoisted = 0;     // literals moved to the __constant__ table
 };
 
 // 4. Shared-memory placement.  A loop-carried value (row, composite cache,
@@ -994,7 +995,7 @@ struct PostStats {
 //    [slot][thread] layout), which frees the registers the unrolled body
 //    needs (at n=40 29 of 68 loop-carried doubles qualify).
 PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, size_t nregions, bool fuse,
-                    int body_region = -1, int threads = 128) {
+                    int body_region = -1, int threads = 128, bool hoist_lits = false) {
   PostStats ps;
   ps.region_ops.assign(nregions, 0.0);
   struct Ln {
@@ -1188,7 +1189,12 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
     std::ostringstream d;
     d << "extern __shared__ __align__(16) unsigned char sm_[];  // loop-carried values the block body never touches\n";
     for (const Mv& m : mv) {
-      d << "#define SM_" << idname[m.id] << " (((" << m.ty << "*)(sm_ + " << off << "))[threadIdx.x])\n";
+      // volatile: without it ptxas forwards every slot store to the slot's
+      // loads and keeps the value in a register anyway (0 LDS in the SASS),
+      // so the placement freed nothing (cplx has no volatile assignment and
+      // stays a plain slot)
+      d << "#define SM_" << idname[m.id] << " (((" << (m.ty == "cplx" ? "" : "volatile ") << m.ty << "*)(sm_ + "
+        << off << "))[threadIdx.x])\n";
       off += m.size * threads;
       moved.insert(m.id);
     }
@@ -1223,15 +1229,92 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
     }
     l.text = t;
   };
+  // ---- 5. hot literals -> __constant__ table.  sm_100a FP64 instructions
+  // take no constant-bank operand: a literal becomes a uniform register
+  // built by two UMOVs at every use (31 % of the executed instructions of the
+  // n=40 bench kernel).  Literals the block body uses at least twice per
+  // iteration go to a __constant__ table instead; ptxas loads those with
+  // LDCU and keeps them in uniform registers across the block loop.  The
+  // table is capped (the 63 uniform registers hold ~31 doubles, and the
+  // UMOV temporaries need some): beyond ~24 entries ptxas spills uniform
+  // registers into the register file.
+  std::string kc_decl;
+  std::unordered_map<std::string, int> kc_index;
+  if (hoist_lits && body_region >= 0 && !getenv("PERM_NO_KC")) {
+    auto lit_at = [](const std::string& t, size_t i, size_t& a, size_t& e) {  // "(0x..p..)" / "(-0x..p..)"
+      if (t[i] != '(') return false;
+      size_t j = i + 1;
+      if (j < t.size() && t[j] == '-') ++j;
+      if (t.compare(j, 2, "0x") != 0) return false;
+      a = j;
+      size_t k = j + 2;
+      while (k < t.size() && (std::isxdigit((unsigned char)t[k]) || t[k] == '.')) ++k;
+      if (k >= t.size() || t[k] != 'p') return false;
+      ++k;
+      if (k < t.size() && (t[k] == '+' || t[k] == '-')) ++k;
+      while (k < t.size() && std::isdigit((unsigned char)t[k])) ++k;
+      if (k >= t.size() || t[k] != ')') return false;
+      e = k;
+      return true;
+    };
+    std::map<std::string, int> cnt;
+    for (const Ln& l : L)
+      if (l.alive && l.region == body_region)
+        for (size_t i = 0, a, e; i < l.text.size(); ++i)
+          if (lit_at(l.text, i, a, e)) {
+            ++cnt[l.text.substr(a, e - a)];
+            i = e;
+          }
+    std::vector<std::pair<int, std::string>> hot;
+    for (auto& kv : cnt)
+      if (kv.second >= 2) hot.push_back({-kv.second, kv.first});
+    std::stable_sort(hot.begin(), hot.end());
+    const int cap = getenv("PERM_KC_CAP") ? atoi(getenv("PERM_KC_CAP")) : 24;
+    if ((int)hot.size() > cap) hot.resize(cap);
+    if (!hot.empty()) {
+      std::ostringstream d;
+      d << "__constant__ double kc_[" << hot.size() << "] = {";
+      for (size_t q = 0; q < hot.size(); ++q) {
+        kc_index[hot[q].second] = (int)q;
+        d << (q ? ", " : "") << hot[q].second;
+      }
+      d << "};  // body literals used >= 2 times per block (LDCU + uniform registers instead of UMOV pairs)\n";
+      kc_decl = d.str();
+      for (Ln& l : L) {
+        if (!l.alive || l.region < 0) continue;
+        std::string t;
+        bool any = false;
+        for (size_t i = 0, a, e; i < l.text.size(); ++i) {
+          if (lit_at(l.text, i, a, e)) {
+            auto it = kc_index.find(l.text.substr(a, e - a));
+            if (it != kc_index.end()) {
+              t += '(';
+              t.append(l.text, i + 1, a - i - 1);  // sign
+              t += "kc_[" + std::to_string(it->second) + "])";
+              i = e;
+              any = true;
+              continue;
+            }
+          }
+          t += l.text[i];
+        }
+        if (any) l.text.swap(t);
+      }
+      ps.hoisted = (int)hot.size();
+    }
+  }
   std::string out;
-  out.reserve(src.size() + smem_decl.size());
+  out.reserve(src.size() + smem_decl.size() + kc_decl.size());
   for (Ln& l : L) {
     if (!l.alive) continue;
     if (!moved.empty()) {
       bool hit = false;
       for (int tk : l.toks) hit |= moved.count(tk) > 0;
       if (hit) rename(l);
-      if (l.text.compare(0, 10, "extern \"C\"") == 0) out += smem_decl;
+    }
+    if (l.text.compare(0, 10, "extern \"C\"") == 0) {
+      out += smem_decl;
+      out += kc_decl;
     }
     out += l.text;
     out += '\n';
@@ -1444,7 +1527,8 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
   (void)ops_switch;
   const bool fuse = !g.i01 && !g.cx && !getenv("PERM_NO_FUSE");
   const int body_region = (U > 0 && nblk > 1) ? (int)g.region_weight.size() - 1 : -1;
-  const PostStats ps = post_pass(kc.source, g.wt, g.region_weight.size(), fuse, body_region, S.threads);
+  const PostStats ps = post_pass(kc.source, g.wt, g.region_weight.size(), fuse, body_region, S.threads,
+                                   !g.i01 && !g.cx);
   kc.smem_bytes = ps.smem_bytes;
   double chunk_ops = 1.0;  // + lacc
   for (size_t k = 0; k < ps.region_ops.size(); ++k) chunk_ops += ps.region_ops[k] * g.region_weight[k];

@@ -639,7 +639,9 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     app(hdr, sizeof hdr);
     // planner knobs read from the environment change plans: part of the key
     for (const char* k : {"PERM_ELIM_CANDS", "PERM_ELIM_MAXSIZE", "PERM_ELIM_BEAM", "PERM_ELIM_VARIANTS", "PERM_NO_CC",
-                          "PERM_PLAN_COMPILES", "PERM_NO_AUTOTUNE", "PERM_ALLOW_SPILL", "PERM_PLAN_BUDGET"}) {
+                          "PERM_PLAN_COMPILES", "PERM_NO_AUTOTUNE", "PERM_ALLOW_SPILL", "PERM_PLAN_BUDGET",
+                          // codegen post-pass knobs (codegen.cpp post_pass)
+                          "PERM_NO_SMEM", "PERM_SMEM_ALL", "PERM_NO_DCE", "PERM_NO_FUSE", "PERM_NO_KC", "PERM_KC_CAP"}) {
       const char* v = getenv(k);
       pkey += k;
       pkey += '=';

@@ -37,11 +37,105 @@ def xf_kc(src):
     return src[:i] + decl + body
 
 
+def xf_hot(src, thr=2, cap=1000):
+    """Body literals used >= thr times per block iteration (at most cap of
+    them, most used first) -> a __constant__ table; ptxas keeps those in
+    uniform registers across the block loop instead of re-materialising each
+    with two UMOVs per use."""
+    import collections
+    L = src.split("\n")
+    bi = max(i for i, l in enumerate(L) if "default: break;" in l) + 2
+    be = max(i for i, l in enumerate(L) if "lacc += cacc" in l)
+    cnt = collections.Counter(m.group(1).lstrip("-") for l in L[bi:be] for m in LIT.finditer(l))
+    hot = [k for k, v in cnt.most_common() if v >= thr][:cap]
+    idx = {k: i for i, k in enumerate(hot)}
+
+    def rep(m):
+        t = m.group(1)
+        a = t.lstrip("-")
+        return f"({'-' if t.startswith('-') else ''}kc_[{idx[a]}])" if a in idx else m.group(0)
+    i = src.index('extern "C"')
+    decl = "__constant__ double kc_[%d] = {%s};\n" % (max(1, len(hot)), ", ".join(hot) or "0")
+    return src[:i] + decl + LIT.sub(rep, src[i:])
+
+
+def xf_vol(src):
+    """shared-memory slots as volatile: ptxas otherwise forwards every SM_
+    store to its loads and keeps the values in registers (0 LDS in SASS)."""
+    return re.sub(r"\(\(\((\w+)\*\)\(sm_ \+ (\d+)\)\)\[threadIdx.x\]\)",
+                  r"(((volatile \1*)(sm_ + \2))[threadIdx.x])", src)
+
+
+def xf_ro(src, vol=True):
+    """loop-carried doubles the block body reads but never writes -> more
+    per-thread shared-memory slots (read with LDS at each body use)."""
+    L = src.split("\n")
+    li = next(i for i, l in enumerate(L) if "for (unsigned blk" in l)
+    bi = max(i for i, l in enumerate(L) if "default: break;" in l) + 2
+    be = max(i for i, l in enumerate(L) if "lacc += cacc" in l)
+    decl = {}
+    for i in range(li - 1, 0, -1):
+        m = re.match(r"\s+double (\w+) = (t\d+|0);$", L[i])
+        if m:
+            decl[m.group(1)] = i
+        elif "const double" in L[i]:
+            break
+    body = "\n".join(L[bi:be])
+    written = set(re.findall(r"^\s+(\w+) = ", body, re.M))
+    used = set(re.findall(r"\b(\w+)\b", body))
+    ro = [v for v in decl if v in used and v not in written and v != "cacc"]
+    offs = [int(x) for x in re.findall(r"\(sm_ \+ (\d+)\)", src)]
+    off = (max(offs) + 1024) if offs else 0
+    thr = int(re.search(r"__launch_bounds__\((\d+)", src).group(1))
+    defs = ""
+    for v in ro:
+        defs += "#define SM_%s (((double*)(sm_ + %d))[threadIdx.x])\n" % (v, off)
+        off += 8 * thr
+    for v in ro:
+        L[decl[v]] = L[decl[v]].replace("double %s =" % v, "SM_%s =" % v)
+    out = "\n".join(L)
+    for v in ro:
+        out = re.sub(r"(?<![\w])%s(?![\w])" % v, "SM_" + v, out)
+        out = out.replace("SM_SM_" + v, "SM_" + v)
+    if "extern __shared__" not in out:
+        out = out.replace('extern "C"', "extern __shared__ __align__(16) unsigned char sm_[];\n" + 'extern "C"', 1)
+    out = out.replace('extern "C"', defs + 'extern "C"', 1)
+    out = out.replace("#define SM_" + ro[0] if ro else "@@", "#define SM_" + ro[0]) if ro else out
+    return (xf_vol(out) if vol else out), off
+
+
+def xf_lb(src, mb):
+    return re.sub(r"__launch_bounds__\((\d+), (\d+)\)", r"__launch_bounds__(\1, %d)" % mb, src)
+
+
 def xf_b64(src):
     return re.sub(r"__launch_bounds__\(128, (\d+)\)", r"__launch_bounds__(64, \1)", src)
 
 
-VARIANTS = {"base": (lambda s: s, 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64)}
+VARIANTS = {"base": (lambda s: s, 128), "hot2": (xf_hot, 128), "hot2c16": (lambda s: xf_hot(s, 2, 16), 128),
+            "hot3": (lambda s: xf_hot(s, 3), 128),
+            "vol": (xf_vol, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
+            "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64)}
+
+
+def variant(name):
+    """'a+b+lb3' composes transforms left to right (lbN: __launch_bounds__ min blocks N)."""
+    fs, threads = [], 128
+    for part in name.split("+"):
+        if part.startswith("lb"):
+            fs.append(lambda s, mb=int(part[2:]): xf_lb(s, mb))
+        else:
+            f, t = VARIANTS[part]
+            fs.append(f)
+            threads = min(threads, t)
+
+    def run(src):
+        smem = None
+        for f in fs:
+            r = f(src)
+            src, smem = r if isinstance(r, tuple) else (r, smem)
+        return (src, smem) if smem is not None else src
+    return run, threads
 
 
 def compile_cubin(src, extra=()):
@@ -65,14 +159,28 @@ def main():
     ap.add_argument("--variants", default="base,kc")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--plan-kw", default="{}", help="JSON dict of extra Plan options")
+    ap.add_argument("--static", action="store_true", help="compile only: print regs/spills per variant (no GPU)")
     a = ap.parse_args()
     import numpy as np
     import torch
     import cuda.bindings.driver as drv
     import synth
     import paper_2501_15126_b200 as pb
-    torch.cuda.init()
     A = synth.erdos_renyi(a.dim, a.p, a.seed)
+    if a.static:
+        P = pb.Plan.from_dense(A, mode="reg", no_device=True, **json.loads(a.plan_kw))
+        for name in a.variants.split(","):
+            s = variant(name)[0](P.source)
+            s, smem = s if isinstance(s, tuple) else (s, P.info["smem_bytes"])
+            cub, regs, spill = compile_cubin(s)
+            with tempfile.NamedTemporaryFile(suffix=".cubin") as f:
+                f.write(cub)
+                f.flush()
+                sass = subprocess.run(["cuobjdump", "-sass", f.name], capture_output=True, text=True).stdout
+            print(json.dumps({"variant": name, "regs": regs, "spill": spill, "smem": smem, "U": P.info["U"],
+                              "umov": sass.count("UMOV "), "lds": sass.count("LDS"), "sts": sass.count("STS")}))
+        return
+    torch.cuda.init()
     P = pb.Plan.from_dense(A, mode="reg", device=0, autotune=-1, **json.loads(a.plan_kw))
     info = P.info
     src = P.source
@@ -85,13 +193,15 @@ def main():
     counter = torch.zeros(64, dtype=torch.int32, device=dev)
     tier = torch.zeros(1 << 20, dtype=torch.float64, device=dev)
     for name in a.variants.split(","):
-        xf, threads = VARIANTS[name]
+        xf, threads = variant(name)
         s = xf(src)
+        smem = info["smem_bytes"]
+        if isinstance(s, tuple):
+            s, smem = s
         cub, regs, spill = compile_cubin(s)
         err, mod = drv.cuModuleLoadData(cub)
         assert err == drv.CUresult.CUDA_SUCCESS, err
         err, fn = drv.cuModuleGetFunction(mod, b"perm_sweep")
-        smem = info["smem_bytes"]
         if smem:
             drv.cuFuncSetAttribute(fn, drv.CUfunction_attribute.CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem)
         err, bps = drv.cuOccupancyMaxActiveBlocksPerMultiprocessor(fn, threads, smem)
