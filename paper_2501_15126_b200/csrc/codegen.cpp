@@ -985,6 +985,7 @@ struct PostStats {
   int smem_bytes = 0;  // per block: loop-carried values moved to shared memory
   int moved = 0;
   int hoisted = 0;     // literals moved to the __constant__ table
+  int vol = 0;         // of the moved values: volatile (really in shared memory)
 };
 
 // 4. Shared-memory placement.  A loop-carried value (row, composite cache,
@@ -995,7 +996,8 @@ struct PostStats {
 //    [slot][thread] layout), which frees the registers the unrolled body
 //    needs (at n=40 29 of 68 loop-carried doubles qualify).
 PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, size_t nregions, bool fuse,
-                    int body_region = -1, int threads = 128, bool hoist_lits = false) {
+                    int body_region = -1, int threads = 128, bool hoist_lits = false,
+                    const std::vector<double>* region_weight = nullptr, double vol_frac_default = 0.5) {
   PostStats ps;
   ps.region_ops.assign(nregions, 0.0);
   struct Ln {
@@ -1188,13 +1190,43 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
     int off = 0;
     std::ostringstream d;
     d << "extern __shared__ __align__(16) unsigned char sm_[];  // loop-carried values the block body never touches\n";
+    // volatile: without it ptxas forwards every slot store to the slot's
+    // loads and keeps the value in a register anyway (0 LDS in the SASS), so
+    // the placement frees nothing.  A volatile slot really lives in shared
+    // memory: an LDS at every read, on the block-boundary path.  So only the
+    // cold slots are volatile: those whose switch-case accesses happen in at
+    // most a fraction vol_frac of the blocks (case j runs in 2^-(j-U+1) of
+    // them); the hot ones stay plain and ptxas keeps them in registers.
+    // cplx slots go through a proxy of two volatile doubles (a volatile
+    // struct has no assignment operator).
+    const double vol_frac = getenv("PERM_SMEM_VOL_FRAC") ? atof(getenv("PERM_SMEM_VOL_FRAC")) : vol_frac_default;
+    std::map<int, double> acc_w;  // value -> executions per chunk of the regions touching it (seed excluded)
+    if (region_weight)
+      for (const Ln& l : L)
+        if (l.alive && l.region > 0 && l.region != body_region && l.region < (int)region_weight->size())
+          for (int t : std::set<int>(l.toks.begin(), l.toks.end())) acc_w[t] += (*region_weight)[l.region];
+    const double body_w =
+        (region_weight && body_region >= 0 && body_region < (int)region_weight->size()) ? (*region_weight)[body_region]
+                                                                                         : 0.0;
+    auto is_vol = [&](int id) {
+      if (vol_frac <= 0 || body_w <= 0) return false;
+      auto it = acc_w.find(id);
+      return (it == acc_w.end() ? 0.0 : it->second) <= vol_frac * body_w * (1 + 1e-9);
+    };
+    bool any_cx = false;
+    for (const Mv& m : mv) any_cx |= m.ty == "cplx" && is_vol(m.id);
+    if (any_cx)
+      d << "struct vcref { volatile double* p;\n"
+           "  __device__ __forceinline__ operator cplx() const { return cplx{p[0], p[1]}; }\n"
+           "  __device__ __forceinline__ void operator=(cplx v) const { p[0] = v.re; p[1] = v.im; } };\n";
     for (const Mv& m : mv) {
-      // volatile: without it ptxas forwards every slot store to the slot's
-      // loads and keeps the value in a register anyway (0 LDS in the SASS),
-      // so the placement freed nothing (cplx has no volatile assignment and
-      // stays a plain slot)
-      d << "#define SM_" << idname[m.id] << " (((" << (m.ty == "cplx" ? "" : "volatile ") << m.ty << "*)(sm_ + "
-        << off << "))[threadIdx.x])\n";
+      const bool vol = is_vol(m.id);
+      ps.vol += vol;
+      if (vol && m.ty == "cplx")
+        d << "#define SM_" << idname[m.id] << " (vcref{((volatile double*)(sm_ + " << off << ")) + 2 * threadIdx.x})\n";
+      else
+        d << "#define SM_" << idname[m.id] << " (((" << (vol ? "volatile " : "") << m.ty << "*)(sm_ + " << off
+          << "))[threadIdx.x])\n";
       off += m.size * threads;
       moved.insert(m.id);
     }
@@ -1528,7 +1560,10 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
   const bool fuse = !g.i01 && !g.cx && !getenv("PERM_NO_FUSE");
   const int body_region = (U > 0 && nblk > 1) ? (int)g.region_weight.size() - 1 : -1;
   const PostStats ps = post_pass(kc.source, g.wt, g.region_weight.size(), fuse, body_region, S.threads,
-                                   !g.i01 && !g.cx);
+                                   !g.i01 && !S.w_only, &g.region_weight,
+                                   // measured on B200 (profiles/r2_smem_vol_ab.txt): real FP64 0.5,
+                                   // INT01 0.125, complex 0 (its 3-block volatile kernels run slower)
+                                   g.cx ? 0.0 : (g.i01 ? 0.125 : 0.5));
   kc.smem_bytes = ps.smem_bytes;
   double chunk_ops = 1.0;  // + lacc
   for (size_t k = 0; k < ps.region_ops.size(); ++k) chunk_ops += ps.region_ops[k] * g.region_weight[k];

@@ -61,6 +61,7 @@ struct KernelSpec {
   bool cc = false;             // composite caches (level/suffix products inside composite roots)
   int min_blocks = 1;          // __launch_bounds__ second argument
   uint64_t nchunks_total = 0;  // 2^(n-1-B)
+  bool w_only = false;         // planner scoring: skip source steps that change neither W nor registers
   // INT01 (internal to generate_kernel): raised register bounds for a regeneration
   const std::map<std::string, double>* reg_lb_extra = nullptr;
 };

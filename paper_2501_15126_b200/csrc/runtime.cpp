@@ -641,7 +641,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     for (const char* k : {"PERM_ELIM_CANDS", "PERM_ELIM_MAXSIZE", "PERM_ELIM_BEAM", "PERM_ELIM_VARIANTS", "PERM_NO_CC",
                           "PERM_PLAN_COMPILES", "PERM_NO_AUTOTUNE", "PERM_ALLOW_SPILL", "PERM_PLAN_BUDGET",
                           // codegen post-pass knobs (codegen.cpp post_pass)
-                          "PERM_NO_SMEM", "PERM_SMEM_ALL", "PERM_NO_DCE", "PERM_NO_FUSE", "PERM_NO_KC", "PERM_KC_CAP"}) {
+                          "PERM_NO_SMEM", "PERM_SMEM_ALL", "PERM_NO_DCE", "PERM_NO_FUSE", "PERM_NO_KC", "PERM_KC_CAP", "PERM_SMEM_VOL_FRAC"}) {
       const char* v = getenv(k);
       pkey += k;
       pkey += '=';
@@ -888,6 +888,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
           sp.mode = PERM_MODE_HYBRID;
           sp.hybrid_c = std::max(std::min(c4 - k, sp.B), std::min(sp.U, sp.B));
         }
+        sp.w_only = true;
         return generate_kernel(o, make_x0(o), sp).w_plan;
       };
       auto evalW = [&, base, ev](const std::vector<int>& s) {
@@ -1019,6 +1020,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
             }
             for (int ccv = 0; ccv < (K > 0 && cc_allowed ? 2 : 1); ++ccv) {
               sp.cc = ccv == 1;
+              sp.w_only = true;
               KernelCode kc = generate_kernel(o, xo, sp);
               // estimates above the 255-register cap are optimistic-capped: ptxas
               // usually fits them (2 blocks of 128); the spill gate escalates if not
@@ -1240,7 +1242,9 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       // start at <= 255 registers (2 blocks/SM: the FP64 pipe is already ~95 %
       // busy there); 3 blocks only for clearly small kernels
       {
-        const int est = generate_kernel(b.o, b.xo, b.sp).est_regs;
+        KernelSpec se = b.sp;
+        se.w_only = true;
+        const int est = generate_kernel(b.o, b.xo, se).est_regs;
         b.sp.min_blocks = p->opts.min_blocks > 0 ? p->opts.min_blocks : std::min(2, bps_of(est + 16, b.sp.threads));
         if (p->opts.min_blocks <= 0 && est + 16 <= 152) b.sp.min_blocks = 3;
       }

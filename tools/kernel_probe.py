@@ -29,6 +29,12 @@ WORKLOADS = {
     "plain_n40_hybrid": (lambda: synth.erdos_renyi(40, 0.2, 1), dict(mode="hybrid", factor_cols=-1)),
     "plain_n36": (lambda: synth.erdos_renyi(36, 0.2, 1), dict(mode="reg", factor_cols=-1)),
     "bench_n40": (lambda: synth.erdos_renyi(40, 0.2, 1), dict(mode="reg")),
+    "c2_n30": (lambda: synth.erdos_renyi(30, 0.3, 1), dict(mode="reg")),
+    "c3_n36": (lambda: synth.erdos_renyi(36, 0.2, 1), dict(mode="reg")),
+    "c3_n36_hybrid": (lambda: synth.erdos_renyi(36, 0.2, 1), dict(mode="hybrid")),
+    "c5_band44_hybrid": (lambda: synth.givens_brickwork(44, 4, 1), dict(mode="hybrid")),
+    "int01_band44": (lambda: (synth.givens_brickwork(44, 4, 1) != 0).astype(float), dict(mode="int01")),
+    "int01_n36": (lambda: synth.erdos_renyi(36, 0.2, 1, binary=True), dict(mode="int01")),
     "band44": (lambda: synth.givens_brickwork(44, 4, 1), dict(mode="reg")),
 }
 
