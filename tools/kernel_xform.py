@@ -104,6 +104,28 @@ def xf_ro(src, vol=True):
     return (xf_vol(out) if vol else out), off
 
 
+def xf_br1(src):
+    """the most frequent block-boundary flip (bit U, every other block) as a
+    direct uniform branch instead of a BRX through the switch's jump table"""
+    m = re.search(r"( +)switch \(j\) \{\n +case (\d+): \{\n", src)
+    if not m:
+        return src
+    ind = m.group(1)
+    head = m.group(0)
+    i = m.start()
+    k = src.index("break; }\n", m.end())
+    k2 = k + len("break; }\n")
+    case_body = src[m.end():k]
+    rest_start = src[k2:]
+    new = (ind + "if (blk & 1u) {  // case %s\n" % m.group(2) + case_body + ind + "} else switch (j) {\n")
+    return src[:i] + new + rest_start
+
+
+def xf_un2(src):
+    """block loop unrolled by 2 (ptxas then sees case U inline on odd blocks)"""
+    return re.sub(r"#pragma unroll 1\n(\s+)for \(unsigned blk", r"#pragma unroll 2\n\1for (unsigned blk", src)
+
+
 def xf_lb(src, mb):
     return re.sub(r"__launch_bounds__\((\d+), (\d+)\)", r"__launch_bounds__(\1, %d)" % mb, src)
 
@@ -114,7 +136,7 @@ def xf_b64(src):
 
 VARIANTS = {"base": (lambda s: s, 128), "hot2": (xf_hot, 128), "hot2c16": (lambda s: xf_hot(s, 2, 16), 128),
             "hot3": (lambda s: xf_hot(s, 3), 128),
-            "vol": (xf_vol, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
+            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
             "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64)}
 
 
