@@ -633,3 +633,35 @@ def test_reseed_interval_caps_the_chunk():
     P = plan(A, reseed_log2=6)
     assert P.info["B"] <= 6
     assert rel(P.compute(), exp) < REL
+
+
+# ---- codegen post-pass variants (DESIGN 3.13(d)/(e)) ---------------------------
+
+@pytest.mark.parametrize("env", [{"PERM_SMEM_VOL_FRAC": "1"}, {"PERM_SMEM_VOL_FRAC": "0"},
+                                 {"PERM_NO_KC": "1"}, {"PERM_SMEM_VOL_FRAC": "1", "PERM_KC_CAP": "8"}])
+def test_post_pass_variants_vs_oracle(env, monkeypatch):
+    """Every shared-memory-slot flavour (all volatile, all plain; the complex
+    volatile proxy) and the literal table on / off / small, in FP64, complex
+    and INT01 kernels with eliminated columns, against the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    A = synth.erdos_renyi(30, 0.2, 2)
+    P = plan(A, mode="reg")
+    src = P.source
+    if env.get("PERM_SMEM_VOL_FRAC") == "1" and P.info["smem_bytes"]:
+        assert "volatile double*" in src
+    if env.get("PERM_NO_KC"):
+        assert "kc_[" not in src
+    exp, _ = oracle.perm_nw(A)
+    assert rel(P.compute(), exp) < REL
+    Z = synth.unitary_brickwork(30, 4, 2)
+    Q = plan(Z)
+    r = Q.compute_ex()
+    got = complex(r.value, r.value_im)
+    exp_z = oracle.perm_band_complex(Z, synth.half_bandwidth(Z))
+    assert abs(got - exp_z) <= 1e-9 * abs(exp_z)
+    if env.get("PERM_SMEM_VOL_FRAC") == "1" and Q.info["smem_bytes"]:
+        assert "vcref" in Q.source
+    B = synth.erdos_renyi(26, 0.25, 2, binary=True)
+    R = plan(B, mode="int01")
+    assert R.exact() == oracle.perm_nw_exact(B)
