@@ -641,7 +641,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     for (const char* k : {"PERM_ELIM_CANDS", "PERM_ELIM_MAXSIZE", "PERM_ELIM_BEAM", "PERM_ELIM_VARIANTS", "PERM_NO_CC",
                           "PERM_PLAN_COMPILES", "PERM_NO_AUTOTUNE", "PERM_ALLOW_SPILL", "PERM_PLAN_BUDGET",
                           // codegen post-pass knobs (codegen.cpp post_pass)
-                          "PERM_NO_SMEM", "PERM_SMEM_ALL", "PERM_NO_DCE", "PERM_NO_FUSE", "PERM_NO_KC", "PERM_KC_CAP", "PERM_SMEM_VOL_FRAC"}) {
+                          "PERM_NO_SMEM", "PERM_SMEM_ALL", "PERM_NO_DCE", "PERM_NO_FUSE", "PERM_NO_KC", "PERM_KC_CAP", "PERM_SMEM_VOL_FRAC", "PERM_LADDER_RUNGS"}) {
       const char* v = getenv(k);
       pkey += k;
       pkey += '=';
@@ -1246,7 +1246,11 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         se.w_only = true;
         const int est = generate_kernel(b.o, b.xo, se).est_regs;
         b.sp.min_blocks = p->opts.min_blocks > 0 ? p->opts.min_blocks : std::min(2, bps_of(est + 16, b.sp.threads));
-        if (p->opts.min_blocks <= 0 && est + 16 <= 152) b.sp.min_blocks = 3;
+        // the estimate misses the composite-evaluation temporaries of
+        // eliminated columns: measured, every K > 0 kernel with est >= 100
+        // spilled hundreds of bytes at the 168-register cap, while K = 0
+        // kernels up to est 102 fit (n = 24-44, ER / band)
+        if (p->opts.min_blocks <= 0 && est + 16 <= 152 && (c.K == 0 || est <= 90)) b.sp.min_blocks = 3;
       }
       // escalation ladder on a spill: a larger register cap (only steps that
       // really raise the __launch_bounds__ cap), then a shorter unrolled block,
@@ -1293,8 +1297,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
           if (cf > 0) t.spill = std::max(t.spill, cf);
         }
         if (getenv("PERM_DEBUG_PLAN"))
-          fprintf(stderr, "[plan]   attempt K %d B %d U %d minb %d cc %d: regs %d stack %d spill %d w %.5f\n", c.K, sp.B,
-                  sp.U, sp.min_blocks, (int)sp.cc, t.regs, t.stack, t.spill, t.kc.w_plan);
+          fprintf(stderr, "[plan]   attempt K %d B %d U %d minb %d cc %d: regs %d stack %d spill %d w %.5f est %d\n", c.K,
+                  sp.B, sp.U, sp.min_blocks, (int)sp.cc, t.regs, t.stack, t.spill, t.kc.w_plan, t.kc.est_regs);
         return t;
       };
       auto take = [&](Att& t) {
@@ -1307,11 +1311,15 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         b.cached = t.cached;
       };
       auto clean = [](const Att& t) { return (t.stack <= 0 && t.spill <= 0) || getenv("PERM_ALLOW_SPILL"); };
-      // the first four rungs compile concurrently (speculatively); the first
+      // the first rungs compile concurrently (speculatively); the first
       // spill-free rung in ladder order wins -- the same choice as compiling
-      // them one after another, in one compile latency instead of four
+      // them one after another, in one compile latency
+      // (two speculative rungs: the first spill-free rung was the first or
+      // second in every measured plan, and the extra rungs only compete for
+      // host cores with the other candidates' compiles)
       std::vector<std::pair<KernelSpec, uint64_t>> ladder = {{b.sp, b.tasks}};
-      while (ladder.size() < 4) {
+      const size_t spec_rungs = getenv("PERM_LADDER_RUNGS") ? (size_t)std::max(1, atoi(getenv("PERM_LADDER_RUNGS"))) : 2;
+      while (ladder.size() < spec_rungs) {
         auto nx = ladder.back();
         if (!escalate(nx.first, nx.second)) break;
         ladder.push_back(nx);
