@@ -17,7 +17,8 @@ def run(name, A, **kw):
     ms = min(P.compute_ex().sweep_ms for _ in range(3))
     i = P.info
     print(json.dumps({"config": name, "n": n, "mode": i["mode"], "K": i["K"], "B": i["B"], "w_plan": i["w_plan"],
-                      "regs": i["regs_per_thread"], "ms": ms, "steps_per_s": (2 ** (n - 1) - 1) / (ms / 1e3),
+                      "U": i["U"], "regs": i["regs_per_thread"],
+                      "blocks_per_sm": i["blocks_per_sm"], "tier_rows": i["tier_rows"], "smem_bytes": i["smem_bytes"], "ms": ms, "steps_per_s": (2 ** (n - 1) - 1) / (ms / 1e3),
                       "value": r.value, "exact": r.exact(), "plan_ms": i["plan_ms"]}), flush=True)
     P.close()
 
@@ -25,10 +26,18 @@ def run(name, A, **kw):
 def main():
     run("C1 n=10 p=0.3 0/1 int01", synth.erdos_renyi(10, 0.3, 1, binary=True), mode="int01")
     run("C2 n=30 p=0.3", synth.erdos_renyi(30, 0.3, 1), mode="reg")
-    run("C3 n=36 p=0.2 hybrid", synth.erdos_renyi(36, 0.2, 1), mode="hybrid")
+    # mode=hybrid asks for Alg. 4's register/global split; after column
+    # elimination the planner leaves no rows for the tier (tier_rows = 0, see
+    # DESIGN 3.5), so the K=0 rows below show the tier itself at work
+    run("C3 n=36 p=0.2 mode=hybrid", synth.erdos_renyi(36, 0.2, 1), mode="hybrid")
+    run("C3 n=36 p=0.2 mode=hybrid K=0 (global tier populated)", synth.erdos_renyi(36, 0.2, 1), mode="hybrid",
+        factor_cols=-1)
+    run("C3 n=36 p=0.2 mode=reg K=0 (shared-memory slots)", synth.erdos_renyi(36, 0.2, 1), mode="reg",
+        factor_cols=-1)
     run("C3 n=36 p=0.2 reg", synth.erdos_renyi(36, 0.2, 1), mode="reg")
     run("C4 n=40 p=0.2", synth.erdos_renyi(40, 0.2, 1), mode="reg")
     run("C5 n=44 band depth 4", synth.givens_brickwork(44, 4, 1), mode="reg")
+    run("C5 n=44 band depth 4 mode=hybrid", synth.givens_brickwork(44, 4, 1), mode="hybrid")
     run("C5' n=44 band U(0,1]", synth.band_positive(44, 4, 1), mode="reg")
     run("0/1 ER n=36 p=0.2 int01", synth.erdos_renyi(36, 0.2, 1, binary=True), mode="int01")
     run("0/1 ER n=36 p=0.2 int01 no zero-skip", synth.erdos_renyi(36, 0.2, 1, binary=True), mode="int01",
