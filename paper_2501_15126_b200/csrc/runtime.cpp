@@ -12,8 +12,10 @@
 #include <cstring>
 #include <future>
 #include <map>
+#include <condition_variable>
 #include <mutex>
 #include <set>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -21,6 +23,33 @@
 
 #include "perm_internal.h"
 #include "plan_state.h"
+
+namespace {
+// Host cores for the planner's CPU work (codegen evaluations, NVRTC): the
+// searches fan out into many std::async tasks (hundreds of threads at the
+// widest beam step); each task holds one slot only while it computes, never
+// while it waits on another task, so the slots bound the CPU contention
+// without any risk of deadlock.
+struct CpuSlots {
+  std::mutex mu;
+  std::condition_variable cv;
+  int free_ = std::max(1u, std::thread::hardware_concurrency());
+  void acquire() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return free_ > 0; });
+    --free_;
+  }
+  void release() {
+    { std::lock_guard<std::mutex> lk(mu); ++free_; }
+    cv.notify_one();
+  }
+};
+CpuSlots g_cpu_slots;
+struct CpuSlot {
+  CpuSlot() { g_cpu_slots.acquire(); }
+  ~CpuSlot() { g_cpu_slots.release(); }
+};
+}  // namespace
 
 extern "C" cudaError_t libperm_launch_tree_reduce(const void* slots, uint64_t count, int kind, void* out,
                                                   void* scratch, cudaStream_t st);
@@ -889,6 +918,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
           sp.hybrid_c = std::max(std::min(c4 - k, sp.B), std::min(sp.U, sp.B));
         }
         sp.w_only = true;
+        CpuSlot slot;
         return generate_kernel(o, make_x0(o), sp).w_plan;
       };
       auto evalW = [&, base, ev](const std::vector<int>& s) {
@@ -1021,7 +1051,11 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
             for (int ccv = 0; ccv < (K > 0 && cc_allowed ? 2 : 1); ++ccv) {
               sp.cc = ccv == 1;
               sp.w_only = true;
-              KernelCode kc = generate_kernel(o, xo, sp);
+              KernelCode kc;
+              {
+                CpuSlot slot;
+                kc = generate_kernel(o, xo, sp);
+              }
               // estimates above the 255-register cap are optimistic-capped: ptxas
               // usually fits them (2 blocks of 128); the spill gate escalates if not
               const double score =
@@ -1286,6 +1320,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
         Att t;
         t.sp = sp;
         t.tasks = tasks;
+        CpuSlot slot;
         t.kc = generate_kernel(b.o, b.xo, sp);
         t.status = nvrtc_compile(t.kc.source, t.cubin, t.log, p->is_u128, t.cached, t.ms);
         if (t.status != PERM_OK) { t.err = g_err; return t; }
