@@ -126,6 +126,33 @@ def xf_un2(src):
     return re.sub(r"#pragma unroll 1\n(\s+)for \(unsigned blk", r"#pragma unroll 2\n\1for (unsigned blk", src)
 
 
+def xf_kcase(src, scope="cases"):
+    """switch-case literals -> a second __constant__ table indexed with a
+    loop-variant zero (blk & (task_stride >> 40)), so ptxas cannot hoist the
+    LDCU loads out of the block loop (uniform-register pressure) and loads
+    them inside the case instead of building each literal with two UMOVs."""
+    L = src.split("\n")
+    si = next(i for i, l in enumerate(L) if "switch (j) {" in l)
+    bi = max(i for i, l in enumerate(L) if "default: break;" in l)
+    be = max(i for i, l in enumerate(L) if "lacc += cacc" in l)
+    lo, hi = (si, bi) if scope == "cases" else (si, be)
+    lits = {}
+
+    def rep(m):
+        t = m.group(1)
+        a = t.lstrip("-")
+        if a not in lits:
+            lits[a] = len(lits)
+        return f"({'-' if t.startswith('-') else ''}kcs_[{lits[a]} + zb_])"
+    for i in range(lo, hi):
+        L[i] = LIT.sub(rep, L[i])
+    li = next(i for i, l in enumerate(L) if "for (unsigned blk" in l)
+    L.insert(li + 1, "        const unsigned zb_ = blk & (unsigned)(task_stride >> 40);")
+    out = "\n".join(L)
+    decl = "__constant__ double kcs_[%d] = {%s};\n" % (max(1, len(lits)), ", ".join(lits) or "0")
+    return out.replace('extern "C"', decl + 'extern "C"', 1)
+
+
 def xf_lb(src, mb):
     return re.sub(r"__launch_bounds__\((\d+), (\d+)\)", r"__launch_bounds__(\1, %d)" % mb, src)
 
@@ -136,7 +163,7 @@ def xf_b64(src):
 
 VARIANTS = {"base": (lambda s: s, 128), "hot2": (xf_hot, 128), "hot2c16": (lambda s: xf_hot(s, 2, 16), 128),
             "hot3": (lambda s: xf_hot(s, 3), 128),
-            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
+            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "kcase": (xf_kcase, 128), "kall": (lambda s: xf_kcase(s, "all"), 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
             "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64)}
 
 
