@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--ordering", default="auto")
     ap.add_argument("--autotune", type=int, default=-1)
+    ap.add_argument("--dump", default="", help="directory: write the plan's kernel source and cubin there")
     a = ap.parse_args()
     import torch
     import paper_2501_15126_b200 as pb
@@ -52,6 +53,10 @@ def main():
     A = make()
     P = pb.Plan.from_dense(A, a.ordering, device=0, autotune=a.autotune, **kw)
     i = P.info
+    if a.dump:
+        os.makedirs(a.dump, exist_ok=True)
+        open(os.path.join(a.dump, a.name + ".cu"), "w").write(P.source)
+        open(os.path.join(a.dump, a.name + ".cubin"), "wb").write(P.cubin())
     P.compute_ex()  # warm-up
     best, r = None, None
     for _ in range(a.reps):

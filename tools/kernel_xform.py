@@ -153,6 +153,33 @@ def xf_kcase(src, scope="cases"):
     return out.replace('extern "C"', decl + 'extern "C"', 1)
 
 
+def xf_pipej(src):
+    """software-pipelined block dispatch: j and s of the NEXT block (BREV/FLO,
+    shifts: MIO latency) are computed before the current block's body, so the
+    dispatch at the loop top only branches; plus the direct branch for the
+    most frequent flip (xf_br1)"""
+    m = re.search(r"( +)#pragma unroll 1\n( +)for \(unsigned blk = 0; blk < (\d+)u; \+\+blk\) \{\n"
+                  r"( +)const unsigned hu = cb \| blk;\n( +)if \(blk != 0\) \{\n"
+                  r"( +)const int j = (\d+) \+ __ffs\(blk\);\n( +)const double s = \(\(hu >> \(j \+ (-?\d+)\)\) & 1u\) \? -1\.0 : 1\.0;\n", src)
+    if not m:
+        return src
+    i0, nb, jb, sh = m.group(1), m.group(3), m.group(7), m.group(9)
+    ind = m.group(4)
+    pre = (f"{i0}unsigned jn_ = {jb} + __ffs(1u);\n{i0}double sn_ = (((cb | 1u) >> (jn_ + {sh})) & 1u) ? -1.0 : 1.0;\n"
+           f"{i0}#pragma unroll 1\n{m.group(2)}for (unsigned blk = 0; blk < {nb}u; ++blk) {{\n"
+           f"{ind}const unsigned hu = cb | blk;\n{m.group(5)}if (blk != 0) {{\n"
+           f"{m.group(6)}const int j = (int)jn_;\n{m.group(8)}const double s = sn_;\n")
+    out = src[:m.start()] + pre + src[m.end():]
+    # next block's dispatch right after the switch (before the body)
+    k = out.index("default: break;")
+    k = out.index("\n", out.index("}", k)) + 1  # end of switch
+    k = out.index("\n", out.index("}", k)) + 1  # end of if (blk != 0)
+    nxt = (f"{ind}{{ const unsigned b1_ = blk + 1u; jn_ = {jb} + __ffs(b1_ | (1u << 30));"
+           f" sn_ = (((cb | b1_) >> (jn_ + {sh})) & 1u) ? -1.0 : 1.0; }}\n")
+    out = out[:k] + nxt + out[k:]
+    return xf_br1(out)
+
+
 def xf_lb(src, mb):
     return re.sub(r"__launch_bounds__\((\d+), (\d+)\)", r"__launch_bounds__(\1, %d)" % mb, src)
 
@@ -163,7 +190,7 @@ def xf_b64(src):
 
 VARIANTS = {"base": (lambda s: s, 128), "hot2": (xf_hot, 128), "hot2c16": (lambda s: xf_hot(s, 2, 16), 128),
             "hot3": (lambda s: xf_hot(s, 3), 128),
-            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "kcase": (xf_kcase, 128), "kall": (lambda s: xf_kcase(s, "all"), 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
+            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "pipej": (xf_pipej, 128), "kcase": (xf_kcase, 128), "kall": (lambda s: xf_kcase(s, "all"), 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
             "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64)}
 
 
@@ -206,6 +233,7 @@ def main():
     ap.add_argument("--p", type=float, default=0.2)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--variants", default="base,kc")
+    ap.add_argument("--workload", default="", help="a tools/kernel_probe.py workload name instead of ER(--dim, --p)")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--plan-kw", default="{}", help="JSON dict of extra Plan options")
     ap.add_argument("--static", action="store_true", help="compile only: print regs/spills per variant (no GPU)")
@@ -216,8 +244,15 @@ def main():
     import synth
     import paper_2501_15126_b200 as pb
     A = synth.erdos_renyi(a.dim, a.p, a.seed)
+    pkw = dict(mode="reg")
+    if a.workload:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from kernel_probe import WORKLOADS
+        make, pkw = WORKLOADS[a.workload]
+        A = make()
+    pkw = {**pkw, **json.loads(a.plan_kw)}
     if a.static:
-        P = pb.Plan.from_dense(A, mode="reg", no_device=True, **json.loads(a.plan_kw))
+        P = pb.Plan.from_dense(A, no_device=True, **pkw)
         for name in a.variants.split(","):
             s = variant(name)[0](P.source)
             s, smem = s if isinstance(s, tuple) else (s, P.info["smem_bytes"])
@@ -230,7 +265,7 @@ def main():
                               "umov": sass.count("UMOV "), "lds": sass.count("LDS"), "sts": sass.count("STS")}))
         return
     torch.cuda.init()
-    P = pb.Plan.from_dense(A, mode="reg", device=0, autotune=-1, **json.loads(a.plan_kw))
+    P = pb.Plan.from_dense(A, device=0, autotune=-1, **pkw)
     info = P.info
     src = P.source
     base_ms = None
@@ -238,7 +273,7 @@ def main():
     dev = torch.device("cuda:0")
     stream = torch.cuda.Stream(device=dev)
     tasks = info["tasks"]
-    slots = torch.zeros(tasks, dtype=torch.float64, device=dev)
+    slots = torch.zeros(tasks * 2, dtype=torch.float64, device=dev)  # complex slots: 2 doubles
     counter = torch.zeros(64, dtype=torch.int32, device=dev)
     tier = torch.zeros(1 << 20, dtype=torch.float64, device=dev)
     for name in a.variants.split(","):
