@@ -49,10 +49,14 @@
 //  * INT01 values are typed int / i64 / wrapping u128 by magnitude bounds; the
 //    chunk loop skips a chunk when its frozen product is 0 on all 32 lanes.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cctype>
 #include <cmath>
 #include <cstring>
 #include <cstdio>
+#include <deque>
+#include <string_view>
 #include <map>
 #include <set>
 #include <sstream>
@@ -978,6 +982,7 @@ struct Gen {
 // 3. The surviving temporaries' instruction weights give the executed DP
 //    instructions per region (W_plan stays equal to ncu's executed count) and
 //    the surviving loop-carried registers give the register estimate.
+std::atomic<long long> g_pp_ns[4];  // post-pass phases: parse, DCE, FMA contraction, placement + output
 struct PostStats {
   std::vector<double> region_ops;
   int reg_words = 0;   // 32-bit words of surviving loop-carried registers
@@ -1000,6 +1005,10 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
                     const std::vector<double>* region_weight = nullptr, double vol_frac_default = 0.5) {
   PostStats ps;
   ps.region_ops.assign(nregions, 0.0);
+  auto tp = [](){ return std::chrono::steady_clock::now(); };
+  auto ns = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return (long long)std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count(); };
+  const auto T0 = tp();
   struct Ln {
     std::string text;
     int region = -1, kind = 0;  // 1 const def, 2 register decl, 3 register assign
@@ -1007,29 +1016,34 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
     std::vector<int> toks;      // identifier ids on the line (all occurrences)
     bool alive = true;
   };
-  std::unordered_map<std::string, int> ids;
-  std::vector<std::string> idname;
-  auto intern = [&](const std::string& s) {
+  // identifiers interned by view (no allocation per token); the names live in
+  // a deque, whose elements never move, so the views stay valid
+  std::unordered_map<std::string_view, int> ids;
+  std::deque<std::string> idname;
+  auto intern = [&](std::string_view s) {
     auto it = ids.find(s);
     if (it != ids.end()) return it->second;
-    ids.emplace(s, (int)idname.size());
-    idname.push_back(s);
+    idname.emplace_back(s);
+    ids.emplace(std::string_view(idname.back()), (int)idname.size() - 1);
     return (int)idname.size() - 1;
   };
   auto isid0 = [](char c) { return std::isalpha((unsigned char)c) || c == '_'; };
   auto isid = [](char c) { return std::isalnum((unsigned char)c) || c == '_'; };
   std::vector<Ln> L;
   {
-    std::istringstream is(src);
-    std::string s;
     int region = -1;
-    while (std::getline(is, s)) {
+    L.reserve(std::count(src.begin(), src.end(), '\n') + 1);
+    for (size_t b = 0; b < src.size();) {
+      size_t e = src.find('\n', b);
+      if (e == std::string::npos) e = src.size();
+      const std::string_view s(src.data() + b, e - b);
+      b = e + 1;
       if (s.compare(0, 3, "//@") == 0) {
-        region = std::atoi(s.c_str() + 4);
+        region = std::atoi(std::string(s.substr(4)).c_str());
         continue;
       }
       Ln l;
-      l.text = s;
+      l.text = std::string(s);
       l.region = region;
       for (size_t i = 0; i < s.size();) {
         if (isid0(s[i]) && (i == 0 || !isid(s[i - 1]))) {
@@ -1046,9 +1060,11 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
       L.push_back(std::move(l));
     }
   }
+  const auto T1 = tp();
+  g_pp_ns[0] += ns(T0, T1);
   std::vector<int> occ(idname.size(), 0), ndef(idname.size(), 0);
   std::vector<char> is_reg(idname.size(), 0);
-  const int id_const = ids.count("const") ? ids["const"] : -2;
+  const int id_const = ids.count("const") ? ids.find("const")->second : -2;
   auto tyword = [&](int id) {
     const std::string& w = idname[id];
     return w == "double" || w == "u128" || w == "cplx" || w == "int" || w == "i64";
@@ -1102,6 +1118,8 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
       }
     }
   }
+  const auto T2 = tp();
+  g_pp_ns[1] += ns(T1, T2);
   if (fuse) {
     std::unordered_map<int, int> def_line;
     std::vector<int> seg(L.size(), 0);
@@ -1171,6 +1189,8 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
       l.text = text;
     }
   }
+  const auto T3 = tp();
+  g_pp_ns[2] += ns(T2, T3);
   // ---- 4. shared-memory placement of values the body never references
   std::set<int> moved;
   std::string smem_decl;
@@ -1360,6 +1380,7 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
     }
   }
   src.swap(out);
+  g_pp_ns[3] += ns(T3, tp());
   if (getenv("PERM_DEBUG_POST"))
     fprintf(stderr, "[post] lines %zu regions %zu removed %d fused %d regwords %d smem %d B (%d values)\n",
             L.size(), nregions, ps.removed, ps.fused, ps.reg_words, ps.smem_bytes, ps.moved);
@@ -1394,8 +1415,26 @@ KernelCode generate_kernel(const Csx& A, const std::vector<double>& x0, const Ke
   }
 }
 
+std::atomic<long long> g_gen_ns{0}, g_post_ns{0}, g_gen_calls{0};
+void codegen_timing(double& gen_ms, double& post_ms, long long& calls) {
+  if (getenv("PERM_DEBUG_TIMING"))
+    fprintf(stderr, "[timing] post-pass phases ms: parse %.1f dce %.1f fuse %.1f place+out %.1f\n", g_pp_ns[0] * 1e-6,
+            g_pp_ns[1] * 1e-6, g_pp_ns[2] * 1e-6, g_pp_ns[3] * 1e-6);
+  gen_ms = g_gen_ns.load() * 1e-6;
+  post_ms = g_post_ns.load() * 1e-6;
+  calls = g_gen_calls.load();
+}
+
 KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, const KernelSpec& S,
                                 std::map<std::string, double>& excess) {
+  const auto t_gen0 = std::chrono::steady_clock::now();
+  struct GenTimer {
+    std::chrono::steady_clock::time_point t0;
+    ~GenTimer() {
+      g_gen_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+      ++g_gen_calls;
+    }
+  } gen_timer{t_gen0};
   Gen g(A, x0, S);
   KernelCode kc;
   const int B = S.B, U = S.U;
@@ -1559,11 +1598,13 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
   (void)ops_switch;
   const bool fuse = !g.i01 && !g.cx && !getenv("PERM_NO_FUSE");
   const int body_region = (U > 0 && nblk > 1) ? (int)g.region_weight.size() - 1 : -1;
+  const auto t_post0 = std::chrono::steady_clock::now();
   const PostStats ps = post_pass(kc.source, g.wt, g.region_weight.size(), fuse, body_region, S.threads,
                                    !g.i01 && !S.w_only, &g.region_weight,
                                    // measured on B200 (profiles/r2_smem_vol_ab.txt): real FP64 0.5,
                                    // INT01 0.125, complex 0 (its 3-block volatile kernels run slower)
                                    g.cx ? 0.0 : (g.i01 ? 0.125 : 0.5));
+  g_post_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_post0).count();
   kc.smem_bytes = ps.smem_bytes;
   double chunk_ops = 1.0;  // + lacc
   for (size_t k = 0; k < ps.region_ops.size(); ++k) chunk_ops += ps.region_ops[k] * g.region_weight[k];

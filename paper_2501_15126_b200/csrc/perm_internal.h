@@ -81,6 +81,9 @@ struct KernelCode {
 // x0 given per ordered row (double; INT01: 2*x0 exactly integral).
 KernelCode generate_kernel(const Csx& occs, const std::vector<double>& x0, const KernelSpec& spec);
 
+// cumulative generate_kernel wall time (all threads), post-pass share, calls
+void codegen_timing(double& gen_ms, double& post_ms, long long& calls);
+
 // Work per Gray step of Alg. 1 as written on this ordered matrix.
 double w_alg1(const Csx& occs);
 

@@ -1498,7 +1498,13 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     }
   }
   I.plan_ms = now_ms() - t0;
-  if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] planning %.3f ms (cached %d)\n", I.plan_ms, I.plan_cached);
+  if (getenv("PERM_DEBUG_TIMING")) {
+    double gms, pms;
+    long long calls;
+    codegen_timing(gms, pms, calls);
+    fprintf(stderr, "[timing] planning %.3f ms (cached %d); generate_kernel %lld calls, %.1f ms summed (post-pass %.1f)\n",
+            I.plan_ms, I.plan_cached, calls, gms, pms);
+  }
   if (!p->opts.no_device) {
     if (ctx_ready.valid()) ctx_ready.wait();
     st = load_device(p);
