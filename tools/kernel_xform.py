@@ -180,6 +180,57 @@ def xf_pipej(src):
     return xf_br1(out)
 
 
+def xf_order(src, how="asap", seed=0):
+    """re-emit the block body's SSA temporaries in another topological order
+    (asap: by dependency depth; alap: as late as possible; rand: random
+    topological order) -- the loop-carried write-backs keep their place at
+    the end; tests how much the source order steers ptxas's schedule"""
+    import random
+    L = src.split("\n")
+    bi = max(i for i, l in enumerate(L) if "default: break;" in l) + 1
+    while L[bi].strip() == "}":
+        bi += 1
+    be = max(i for i, l in enumerate(L) if "lacc += cacc" in l)
+    body = L[bi:be]
+    defs, rest = [], []
+    for l in body:
+        (defs if re.match(r"\s+const (double|int|u128|i64|cplx) t\d+ = ", l) else rest).append(l)
+    # the block's sign line etc. (non-SSA) stay in front, write-backs after
+    head = [l for l in rest if "sU" in l and "const" in l]
+    tailr = [l for l in rest if l not in head]
+    name = [re.match(r"\s+const \w+ (t\d+) = ", l).group(1) for l in defs]
+    idx = {v: k for k, v in enumerate(name)}
+    deps = [[idx[t] for t in re.findall(r"\b(t\d+)\b", l.split(" = ", 1)[1]) if t in idx] for l in defs]
+    users = [[] for _ in defs]
+    for k, ds in enumerate(deps):
+        for d in ds:
+            users[d].append(k)
+    n = len(defs)
+    if how == "asap":
+        depth = [0] * n
+        for k in range(n):
+            depth[k] = 1 + max([depth[d] for d in deps[k]], default=0)
+        order = sorted(range(n), key=lambda k: (depth[k], k))
+    elif how == "alap":
+        h = [0] * n
+        for k in reversed(range(n)):
+            h[k] = 1 + max([h[u] for u in users[k]], default=0)
+        order = sorted(range(n), key=lambda k: (-h[k], k))
+    else:
+        rnd = random.Random(seed)
+        indeg = [len(set(d)) for d in deps]
+        ready = [k for k in range(n) if indeg[k] == 0]
+        order = []
+        while ready:
+            k = ready.pop(rnd.randrange(len(ready)))
+            order.append(k)
+            for u in set(users[k]):
+                indeg[u] -= 1
+                if indeg[u] == 0:
+                    ready.append(u)
+    return "\n".join(L[:bi] + head + [defs[k] for k in order] + tailr + L[be:])
+
+
 def xf_lb(src, mb):
     return re.sub(r"__launch_bounds__\((\d+), (\d+)\)", r"__launch_bounds__(\1, %d)" % mb, src)
 
@@ -190,7 +241,9 @@ def xf_b64(src):
 
 VARIANTS = {"base": (lambda s: s, 128), "hot2": (xf_hot, 128), "hot2c16": (lambda s: xf_hot(s, 2, 16), 128),
             "hot3": (lambda s: xf_hot(s, 3), 128),
-            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "pipej": (xf_pipej, 128), "kcase": (xf_kcase, 128), "kall": (lambda s: xf_kcase(s, "all"), 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
+            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "asap": (lambda s: xf_order(s, "asap"), 128),
+            "alap": (lambda s: xf_order(s, "alap"), 128), "rand1": (lambda s: xf_order(s, "rand", 1), 128),
+            "rand2": (lambda s: xf_order(s, "rand", 2), 128), "rand3": (lambda s: xf_order(s, "rand", 3), 128), "pipej": (xf_pipej, 128), "kcase": (xf_kcase, 128), "kall": (lambda s: xf_kcase(s, "all"), 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
             "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64)}
 
 
