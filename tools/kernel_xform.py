@@ -231,6 +231,39 @@ def xf_order(src, how="asap", seed=0):
     return "\n".join(L[:bi] + head + [defs[k] for k in order] + tailr + L[be:])
 
 
+MUL_S32_U128 = r"""
+__device__ __forceinline__ u128 mul_s32_u128(int b, u128 a) {
+  unsigned a0 = (unsigned)a, a1 = (unsigned)(a >> 32), a2 = (unsigned)(a >> 64), a3 = (unsigned)(a >> 96);
+  unsigned r0, r1, r2, r3;
+  const unsigned ub = (unsigned)b, m = (unsigned)(b >> 31);
+  asm("mul.lo.u32 %0, %4, %8;\n\tmul.hi.u32 %1, %4, %8;\n\tmad.lo.cc.u32 %1, %5, %8, %1;\n\t"
+      "madc.hi.u32 %2, %5, %8, 0;\n\tmad.lo.cc.u32 %2, %6, %8, %2;\n\tmadc.hi.u32 %3, %6, %8, 0;\n\t"
+      "mad.lo.u32 %3, %7, %8, %3;\n\tand.b32 %4, %4, %9;\n\tand.b32 %5, %5, %9;\n\tand.b32 %6, %6, %9;\n\t"
+      "sub.cc.u32 %1, %1, %4;\n\tsubc.cc.u32 %2, %2, %5;\n\tsubc.u32 %3, %3, %6;"
+      : "=&r"(r0), "=&r"(r1), "=&r"(r2), "=&r"(r3), "+r"(a0), "+r"(a1), "+r"(a2) : "r"(a3), "r"(ub), "r"(m));
+  return ((u128)(((unsigned long long)r3 << 32) | r2) << 64) | (((unsigned long long)r1 << 32) | r0);
+}
+"""
+
+
+def xf_m128(src):
+    """INT01: (u128)(i128)int * u128 through a hand-scheduled 32 x 128-bit
+    multiply (4 wide multiplies + masked correction for a negative int)"""
+    ty = {m.group(2): m.group(1) for m in re.finditer(r"(?:const )?(int|i64|u128) (\w+) = ", src)}
+    pat = re.compile(r"\(u128\)\(i128\)(\w+) \* (\w+)|(\w+) \* \(u128\)\(i128\)(\w+)")
+
+    def rep(m):
+        if m.group(1):
+            nar, wide = m.group(1), m.group(2)
+        else:
+            wide, nar = m.group(3), m.group(4)
+        if ty.get(nar) == "int" and ty.get(wide) == "u128":
+            return f"mul_s32_u128({nar}, {wide})"
+        return m.group(0)
+    out = pat.sub(rep, src)
+    return out.replace('extern "C"', MUL_S32_U128 + 'extern "C"', 1)
+
+
 def xf_lb(src, mb):
     return re.sub(r"__launch_bounds__\((\d+), (\d+)\)", r"__launch_bounds__(\1, %d)" % mb, src)
 
@@ -241,7 +274,7 @@ def xf_b64(src):
 
 VARIANTS = {"base": (lambda s: s, 128), "hot2": (xf_hot, 128), "hot2c16": (lambda s: xf_hot(s, 2, 16), 128),
             "hot3": (lambda s: xf_hot(s, 3), 128),
-            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "asap": (lambda s: xf_order(s, "asap"), 128),
+            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "m128": (xf_m128, 128), "asap": (lambda s: xf_order(s, "asap"), 128),
             "alap": (lambda s: xf_order(s, "alap"), 128), "rand1": (lambda s: xf_order(s, "rand", 1), 128),
             "rand2": (lambda s: xf_order(s, "rand", 2), 128), "rand3": (lambda s: xf_order(s, "rand", 3), 128), "pipej": (xf_pipej, 128), "kcase": (xf_kcase, 128), "kall": (lambda s: xf_kcase(s, "all"), 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
             "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64)}
