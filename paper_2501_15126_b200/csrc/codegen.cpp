@@ -101,6 +101,7 @@ struct Gen {
   const KernelSpec& S;
   const std::vector<double>& x0;
   const bool i01;
+  bool asm_mul = false;                  // INT01: int x u128 products via mul_s32_u128
   int n, K, B, U;
   std::vector<Factor> fac;
   std::vector<int> fac_of_row;
@@ -140,6 +141,7 @@ struct Gen {
 
   Gen(const Csx& a, const std::vector<double>& x, const KernelSpec& s)
       : A(a), S(s), x0(x), i01(s.mode == PERM_MODE_INT01), n(a.n), K(s.K), B(s.B), U(s.U) {
+    asm_mul = i01 && s.i01_asm_mul;
     cx = S.mode == PERM_MODE_COMPLEX_INTERNAL;
     colval.assign(n, {});
     for (int j = 0; j < n; ++j)
@@ -457,7 +459,13 @@ struct Gen {
       switch (op) {
         case '+': expr = icast(a, rt) + " + " + icast(b, rt); break;
         case '-': expr = icast(a, rt) + " - " + icast(b, rt); break;
-        case '*': expr = icast(a, rt) + " * " + icast(b, rt); break;
+        case '*':
+          if (rt == 'u' && asm_mul && ((vals[a].ty == 'i' && vals[b].ty == 'u') || (vals[b].ty == 'i' && vals[a].ty == 'u')))
+            expr = vals[a].ty == 'i' ? "mul_s32_u128(" + nm(a) + ", " + nm(b) + ")"
+                                     : "mul_s32_u128(" + nm(b) + ", " + nm(a) + ")";
+          else
+            expr = icast(a, rt) + " * " + icast(b, rt);
+          break;
         case 'h': expr = "2 * " + icast(a, rt); break;
       }
       ops += w;
@@ -1461,6 +1469,22 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
          "__device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx c) {\n"
          "  return cplx{fma(a.re, b.re, fma(-a.im, b.im, c.re)), fma(a.re, b.im, fma(a.im, b.re, c.im))}; }\n";
   if (g.i01) o << "typedef unsigned __int128 u128;\ntypedef __int128 i128;\ntypedef long long i64;\n";
+  if (g.i01 && S.i01_asm_mul)
+    // a * b mod 2^128 for a signed 32-bit b: a * (uint32)b as four 32x32
+    // partial products chained through the carry flag, minus (a << 32) when
+    // b < 0 (~12 integer instructions; nvcc's generic sign-extended 128-bit
+    // multiply is ~17)
+    o << "__device__ __forceinline__ u128 mul_s32_u128(int b, u128 a) {\n"
+         "  unsigned a0 = (unsigned)a, a1 = (unsigned)(a >> 32), a2 = (unsigned)(a >> 64), a3 = (unsigned)(a >> 96);\n"
+         "  unsigned r0, r1, r2, r3;\n"
+         "  const unsigned ub = (unsigned)b, m = (unsigned)(b >> 31);\n"
+         "  asm(\"mul.lo.u32 %0, %4, %8;\\n\\tmul.hi.u32 %1, %4, %8;\\n\\tmad.lo.cc.u32 %1, %5, %8, %1;\\n\\t\"\n"
+         "      \"madc.hi.u32 %2, %5, %8, 0;\\n\\tmad.lo.cc.u32 %2, %6, %8, %2;\\n\\tmadc.hi.u32 %3, %6, %8, 0;\\n\\t\"\n"
+         "      \"mad.lo.u32 %3, %7, %8, %3;\\n\\tand.b32 %4, %4, %9;\\n\\tand.b32 %5, %5, %9;\\n\\tand.b32 %6, %6, %9;\\n\\t\"\n"
+         "      \"sub.cc.u32 %1, %1, %4;\\n\\tsubc.cc.u32 %2, %2, %5;\\n\\tsubc.u32 %3, %3, %6;\"\n"
+         "      : \"=&r\"(r0), \"=&r\"(r1), \"=&r\"(r2), \"=&r\"(r3), \"+r\"(a0), \"+r\"(a1), \"+r\"(a2) : \"r\"(a3), \"r\"(ub), \"r\"(m));\n"
+         "  return ((u128)(((unsigned long long)r3 << 32) | r2) << 64) | (((unsigned long long)r1 << 32) | r0);\n"
+         "}\n";
   // HYBRID tier: the paper's coalesced x[nthreads * row + tid] layout (Listing 4,
   // P:543-550), vectorised: row slots 2p, 2p+1 of a thread form one double2
   // (int2) at pair index p * (all threads) + thread; complex rows: one cplx each

@@ -62,6 +62,7 @@ struct KernelSpec {
   int min_blocks = 1;          // __launch_bounds__ second argument
   uint64_t nchunks_total = 0;  // 2^(n-1-B)
   bool w_only = false;         // planner scoring: skip source steps that change neither W nor registers
+  bool i01_asm_mul = false;    // INT01: int x u128 products through the hand-scheduled mul_s32_u128
   // INT01 (internal to generate_kernel): raised register bounds for a regeneration
   const std::map<std::string, double>* reg_lb_extra = nullptr;
 };

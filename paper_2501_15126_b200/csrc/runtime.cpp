@@ -670,7 +670,8 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     for (const char* k : {"PERM_ELIM_CANDS", "PERM_ELIM_MAXSIZE", "PERM_ELIM_BEAM", "PERM_ELIM_VARIANTS", "PERM_NO_CC",
                           "PERM_PLAN_COMPILES", "PERM_NO_AUTOTUNE", "PERM_ALLOW_SPILL", "PERM_PLAN_BUDGET",
                           // codegen post-pass knobs (codegen.cpp post_pass)
-                          "PERM_NO_SMEM", "PERM_SMEM_ALL", "PERM_NO_DCE", "PERM_NO_FUSE", "PERM_NO_KC", "PERM_KC_CAP", "PERM_SMEM_VOL_FRAC", "PERM_LADDER_RUNGS"}) {
+                          "PERM_NO_SMEM", "PERM_SMEM_ALL", "PERM_NO_DCE", "PERM_NO_FUSE", "PERM_NO_KC", "PERM_KC_CAP", "PERM_SMEM_VOL_FRAC", "PERM_LADDER_RUNGS",
+                          "PERM_NO_ASM_MUL", "PERM_ASM_MUL"}) {
       const char* v = getenv(k);
       pkey += k;
       pkey += '=';
@@ -1271,6 +1272,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       b.o = permute_ccs(p->ccs, b.rp, b.colp);
       b.xo = make_x0(b.o);
       b.sp.cc = c.cc;
+      b.sp.i01_asm_mul = getenv("PERM_ASM_MUL") && atoi(getenv("PERM_ASM_MUL")) == 1;
       set_hybrid(b.sp, b.o);
       if (n == 1 || p->singular) { b.ok = true; return b; }
       // start at <= 255 registers (2 blocks/SM: the FP64 pipe is already ~95 %
@@ -1421,8 +1423,42 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     size_t pick = 0;
     for (size_t q = 1; q < oks.size(); ++q)
       if (oks[q].score < oks[pick].score) pick = q;
-    if (oks.size() > 1 && !p->opts.no_device && p->opts.autotune >= 0 &&
-        !(getenv("PERM_NO_AUTOTUNE") && atoi(getenv("PERM_NO_AUTOTUNE")))) {
+    const bool measured = !p->opts.no_device && p->opts.autotune >= 0 &&
+                          !(getenv("PERM_NO_AUTOTUNE") && atoi(getenv("PERM_NO_AUTOTUNE")));
+    // INT01 with on-device autotune: the model's pick also with the
+    // hand-scheduled int x u128 multiply (DESIGN 3.9) -- same spec, one more
+    // compile.  It wins on some kernels (0/1 ER n=40: 14.6 -> 12.8 ms) and
+    // loses on others (0/1 band n=44: 1.22 -> 1.31 ms), which only a
+    // measurement tells apart; the model pick alone keeps nvcc's multiply.
+    if (mode == PERM_MODE_INT01 && measured && !oks.empty() && !oks[pick].b.sp.i01_asm_mul &&
+        !getenv("PERM_NO_ASM_MUL")) {
+      Ok alt{oks[pick].score, oks[pick].ci, oks[pick].b};
+      Built& b = alt.b;
+      b.sp.i01_asm_mul = true;
+      {
+        CpuSlot slot;
+        b.kc = generate_kernel(b.o, b.xo, b.sp);
+      }
+      double ms = 0;
+      bool cached = false;
+      b.cubin.clear();
+      if (nvrtc_compile(b.kc.source, b.cubin, b.log, p->is_u128, cached, ms) == PERM_OK) {
+        int regs = -1, stack = 0, spill = 0, cr = -1, cf = -1;
+        parse_ptxas(b.log, regs, stack, spill);
+        if (cubin_attrs(b.cubin, cr, cf)) {
+          regs = cr;
+          stack = std::max(stack, cf);
+          spill = std::max(spill, cf);
+        }
+        I.nvrtc_cpu_ms += ms;
+        if (stack <= 0 && spill <= 0) {
+          b.regs = regs;
+          b.cached = cached;
+          oks.push_back(std::move(alt));
+        }
+      }
+    }
+    if (oks.size() > 1 && measured) {
       std::vector<const Built*> bs;
       std::vector<double> pskips;
       for (const Ok& o : oks) {

@@ -665,3 +665,22 @@ def test_post_pass_variants_vs_oracle(env, monkeypatch):
     B = synth.erdos_renyi(26, 0.25, 2, binary=True)
     R = plan(B, mode="int01")
     assert R.exact() == oracle.perm_nw_exact(B)
+
+
+@pytest.mark.parametrize("n,p,seed", [(24, 0.25, 1), (30, 0.2, 2), (32, 0.2, 3)])
+def test_int01_asm_multiply_bit_exact(n, p, seed, monkeypatch):
+    """INT01 with the hand-scheduled signed 32 x 128-bit multiply (the
+    autotune candidate of DESIGN 3.9) forced on every kernel: bit-exact
+    against the oracle (doubled row values are negative half the time, so the
+    sign correction is exercised)."""
+    monkeypatch.setenv("PERM_ASM_MUL", "1")
+    B = synth.erdos_renyi(n, p, seed, binary=True)
+    P = plan(B, mode="int01")
+    assert "mul_s32_u128(" in P.source
+    assert P.exact() == oracle.perm_nw_exact(B)
+
+
+def test_int01_autotune_with_asm_candidate_bit_exact():
+    B = synth.erdos_renyi(34, 0.2, 1, binary=True)
+    P = plan(B, mode="int01", autotune=0)
+    assert P.exact() == oracle.perm_nw_exact(B)

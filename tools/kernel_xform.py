@@ -246,7 +246,22 @@ __device__ __forceinline__ u128 mul_s32_u128(int b, u128 a) {
 """
 
 
-def xf_m128(src):
+MUL_S32_U128_C = r"""
+__device__ __forceinline__ u128 mul_s32_u128(int b, u128 a) {
+  typedef unsigned long long u64_;
+  const unsigned ub = (unsigned)b, m = (unsigned)(b >> 31);
+  const unsigned a0 = (unsigned)a, a1 = (unsigned)(a >> 32), a2 = (unsigned)(a >> 64), a3 = (unsigned)(a >> 96);
+  const u64_ p0 = (u64_)a0 * ub;
+  const u64_ p1 = (u64_)a1 * ub + (p0 >> 32);
+  const u64_ p2 = (u64_)a2 * ub + (p1 >> 32);
+  const unsigned r3 = a3 * ub + (unsigned)(p2 >> 32);
+  const u128 r = ((u128)(((u64_)r3 << 32) | (unsigned)p2) << 64) | ((p1 << 32) | (unsigned)p0);
+  return r - ((u128)((((u64_)(a1 & m)) << 32) | (a0 & m)) << 32 | ((u128)(a2 & m) << 96));
+}
+"""
+
+
+def xf_m128(src, helper=None):
     """INT01: (u128)(i128)int * u128 through a hand-scheduled 32 x 128-bit
     multiply (4 wide multiplies + masked correction for a negative int)"""
     ty = {m.group(2): m.group(1) for m in re.finditer(r"(?:const )?(int|i64|u128) (\w+) = ", src)}
@@ -261,7 +276,7 @@ def xf_m128(src):
             return f"mul_s32_u128({nar}, {wide})"
         return m.group(0)
     out = pat.sub(rep, src)
-    return out.replace('extern "C"', MUL_S32_U128 + 'extern "C"', 1)
+    return out.replace('extern "C"', (helper or MUL_S32_U128) + 'extern "C"', 1)
 
 
 def xf_lb(src, mb):
@@ -274,7 +289,7 @@ def xf_b64(src):
 
 VARIANTS = {"base": (lambda s: s, 128), "hot2": (xf_hot, 128), "hot2c16": (lambda s: xf_hot(s, 2, 16), 128),
             "hot3": (lambda s: xf_hot(s, 3), 128),
-            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "m128": (xf_m128, 128), "asap": (lambda s: xf_order(s, "asap"), 128),
+            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "m128": (xf_m128, 128), "m128c": (lambda s: xf_m128(s, MUL_S32_U128_C), 128), "asap": (lambda s: xf_order(s, "asap"), 128),
             "alap": (lambda s: xf_order(s, "alap"), 128), "rand1": (lambda s: xf_order(s, "rand", 1), 128),
             "rand2": (lambda s: xf_order(s, "rand", 2), 128), "rand3": (lambda s: xf_order(s, "rand", 3), 128), "pipej": (xf_pipej, 128), "kcase": (xf_kcase, 128), "kall": (lambda s: xf_kcase(s, "all"), 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
             "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64)}
