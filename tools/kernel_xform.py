@@ -261,6 +261,50 @@ __device__ __forceinline__ u128 mul_s32_u128(int b, u128 a) {
 """
 
 
+MUL_U128 = r"""
+__device__ __forceinline__ u128 mul_u128(u128 a, u128 b) {
+  const unsigned a0 = (unsigned)a, a1 = (unsigned)(a >> 32), a2 = (unsigned)(a >> 64), a3 = (unsigned)(a >> 96);
+  const unsigned b0 = (unsigned)b, b1 = (unsigned)(b >> 32), b2 = (unsigned)(b >> 64), b3 = (unsigned)(b >> 96);
+  unsigned r0, r1, r2, r3;
+  asm("mul.lo.u32 %0, %4, %8;\n\t"
+      "mul.hi.u32 %1, %4, %8;\n\t"
+      "mad.lo.cc.u32 %1, %4, %9, %1;\n\t"
+      "madc.hi.u32 %2, %4, %9, 0;\n\t"
+      "mad.lo.cc.u32 %1, %5, %8, %1;\n\t"
+      "madc.hi.cc.u32 %2, %5, %8, %2;\n\t"
+      "addc.u32 %3, 0, 0;\n\t"
+      "mad.lo.cc.u32 %2, %4, %10, %2;\n\t"
+      "madc.hi.u32 %3, %4, %10, %3;\n\t"
+      "mad.lo.cc.u32 %2, %5, %9, %2;\n\t"
+      "madc.hi.u32 %3, %5, %9, %3;\n\t"
+      "mad.lo.cc.u32 %2, %6, %8, %2;\n\t"
+      "madc.hi.u32 %3, %6, %8, %3;\n\t"
+      "mad.lo.u32 %3, %4, %11, %3;\n\t"
+      "mad.lo.u32 %3, %5, %10, %3;\n\t"
+      "mad.lo.u32 %3, %6, %9, %3;\n\t"
+      "mad.lo.u32 %3, %7, %8, %3;"
+      : "=&r"(r0), "=&r"(r1), "=&r"(r2), "=&r"(r3)
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(b2), "r"(b3));
+  return ((u128)(((unsigned long long)r3 << 32) | r2) << 64) | (((unsigned long long)r1 << 32) | r0);
+}
+"""
+
+
+def xf_m128u(src):
+    """INT01: u128 x u128 products through a hand-scheduled schoolbook
+    multiply (mod 2^128), on top of xf_m128"""
+    out = xf_m128(src)
+    ty = {m.group(2): m.group(1) for m in re.finditer(r"(?:const )?(int|i64|u128) (\w+) = ", src)}
+
+    def rep(m):
+        a, b = m.group(1), m.group(2)
+        if ty.get(a) == "u128" and ty.get(b) == "u128":
+            return f"mul_u128({a}, {b})"
+        return m.group(0)
+    out = re.sub(r"\b(\w+) \* (\w+)\b(?!\()", rep, out)
+    return out.replace("__device__ __forceinline__ u128 mul_s32_u128", MUL_U128 + "__device__ __forceinline__ u128 mul_s32_u128", 1)
+
+
 def xf_m128(src, helper=None):
     """INT01: (u128)(i128)int * u128 through a hand-scheduled 32 x 128-bit
     multiply (4 wide multiplies + masked correction for a negative int)"""
@@ -289,7 +333,7 @@ def xf_b64(src):
 
 VARIANTS = {"base": (lambda s: s, 128), "hot2": (xf_hot, 128), "hot2c16": (lambda s: xf_hot(s, 2, 16), 128),
             "hot3": (lambda s: xf_hot(s, 3), 128),
-            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "m128": (xf_m128, 128), "m128c": (lambda s: xf_m128(s, MUL_S32_U128_C), 128), "asap": (lambda s: xf_order(s, "asap"), 128),
+            "vol": (xf_vol, 128), "br1": (xf_br1, 128), "m128": (xf_m128, 128), "m128u": (xf_m128u, 128), "m128c": (lambda s: xf_m128(s, MUL_S32_U128_C), 128), "asap": (lambda s: xf_order(s, "asap"), 128),
             "alap": (lambda s: xf_order(s, "alap"), 128), "rand1": (lambda s: xf_order(s, "rand", 1), 128),
             "rand2": (lambda s: xf_order(s, "rand", 2), 128), "rand3": (lambda s: xf_order(s, "rand", 3), 128), "pipej": (xf_pipej, 128), "kcase": (xf_kcase, 128), "kall": (lambda s: xf_kcase(s, "all"), 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
             "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64)}

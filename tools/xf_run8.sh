@@ -1,4 +1,4 @@
-for w in int01_n40 int01_n36 int01_band44; do python tools/kernel_xform.py --workload $w --variants base,m128,m128c --reps 7 >> gpurun_out/xf8.jsonl 2>>gpurun_out/xf8.err; done
+for w in int01_n40 int01_n36 int01_band44; do python tools/kernel_xform.py --workload $w --variants base,m128,m128u --reps 7 >> gpurun_out/xf8.jsonl 2>>gpurun_out/xf8.err; done
 python -c "
 import json
 for l in open('gpurun_out/xf8.jsonl'):
