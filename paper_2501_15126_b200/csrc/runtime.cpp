@@ -12,6 +12,7 @@
 #include <cstring>
 #include <future>
 #include <map>
+#include <memory>
 #include <condition_variable>
 #include <mutex>
 #include <set>
@@ -21,10 +22,21 @@
 
 #include <unistd.h>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a profiler is attached
+
 #include "perm_internal.h"
 #include "plan_state.h"
 
 namespace {
+// NVTX ranges around the planner phases and the compute steps (nsys / ncu
+// timelines; `ncu --nvtx --nvtx-include perm_compute/` selects one permanent)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
+
 // Host cores for the planner's CPU work (codegen evaluations, NVRTC): the
 // searches fan out into many std::async tasks (hundreds of threads at the
 // widest beam step); each task holds one slot only while it computes, never
@@ -401,10 +413,16 @@ int run_range(perm_plan_s* p, uint64_t first, uint64_t count, double* sweep_ms, 
   const int grid = (int)std::min<uint64_t>((uint64_t)p->info.grid,
                                            (count * 32 + p->spec.threads - 1) / p->spec.threads);
   CUDA_TRY(cudaEventRecord(p->ev[0], p->stream));
-  CUDA_TRY(cudaLaunchKernel((const void*)p->kern, dim3(grid), dim3(p->spec.threads), args,
-                            (size_t)p->code.smem_bytes, p->stream));
+  {
+    Nvtx r("perm_sweep");
+    CUDA_TRY(cudaLaunchKernel((const void*)p->kern, dim3(grid), dim3(p->spec.threads), args,
+                              (size_t)p->code.smem_bytes, p->stream));
+  }
   CUDA_TRY(cudaEventRecord(p->ev[1], p->stream));
-  CUDA_TRY(libperm_launch_tree_reduce(p->d_slots, count, p->kind(), p->d_partial, p->d_rscratch, p->stream));
+  {
+    Nvtx r("perm_reduce");
+    CUDA_TRY(libperm_launch_tree_reduce(p->d_slots, count, p->kind(), p->d_partial, p->d_rscratch, p->stream));
+  }
   CUDA_TRY(cudaEventRecord(p->ev[2], p->stream));
   if (sweep_ms || reduce_ms) {
     CUDA_TRY(cudaEventSynchronize(p->ev[2]));
@@ -512,6 +530,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
                      bool complex_input, perm_ordering ord, const perm_opts* opts_in, perm_plan_t* out) {
   if (!out) return fail(PERM_EINVAL, "out is NULL");
   *out = nullptr;
+  Nvtx range("perm_plan");
   const double t0 = now_ms();
   auto* p = new perm_plan_s();
   if (opts_in) p->opts = *opts_in;
@@ -995,6 +1014,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     const bool tiers = !getenv("PERM_ELIM_MAXSIZE");  // every mode: FP64, INT01, complex
     const int nev = getenv("PERM_ELIM_VARIANTS") ? std::max(1, atoi(getenv("PERM_ELIM_VARIANTS"))) : (tiers ? 18 : 6);
     {
+      Nvtx r_search("perm_plan/search");
       std::vector<std::pair<int, std::future<std::vector<int>>>> runs;  // greedy runs, concurrently
       for (int base : bases)
         for (int ev = 0; ev < nev; ++ev) {
@@ -1386,6 +1406,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     std::vector<Ok> oks;
     const double t_compile0 = now_ms();
     I.codegen_ms = t_compile0 - tc;
+    auto nvrtc_range = std::make_unique<Nvtx>("perm_plan/nvrtc");  // popped below or on an early return
     std::vector<std::future<Built>> fut;  // candidates compiled concurrently (NVRTC is thread-safe)
     for (const Cand& c : cands) fut.push_back(std::async(std::launch::async, build, c));
     for (size_t ci = 0; ci < cands.size(); ++ci) {
@@ -1415,6 +1436,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       oks.push_back({score, ci, std::move(b)});
     }
     I.nvrtc_ms = now_ms() - t_compile0;
+    nvrtc_range.reset();
     if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] compiles %.3f ms (%zu)\n", now_ms() - tc, oks.size());
     // model choice; then, with a device, measured choice (autotune): each
     // compiled candidate sweeps a few spread samples of its task range, and
@@ -1736,6 +1758,7 @@ int perm_compute_async(perm_plan_t p, void* d_out) {
   if (world > 128) return fail(PERM_EINVAL, "world > 128");
   if (world > 1 && !p->opts.nccl_comm) return fail(PERM_EINVAL, "opts.world > 1 needs opts.nccl_comm");
   const size_t pb = p->pbytes();
+  Nvtx range("perm_compute");
   CUDA_TRY(cudaSetDevice(p->device));
   // this rank's unscaled partial into its slot of the gather buffer
   char* gather = static_cast<char*>(p->d_scratch);
@@ -1743,10 +1766,14 @@ int perm_compute_async(perm_plan_t p, void* d_out) {
   if (st) return st;
   if (p->opts.nccl_comm) {  // the path's one exchange step (in-place all-gather)
     std::string msg;
+    Nvtx r("perm_allgather");
     st = libperm_allgather(p->opts.nccl_comm, gather, pb, rank, p->stream, msg);
     if (st) return fail(st, msg);
   }
-  st = perm_fold_async(p, gather, world, d_out);
+  {
+    Nvtx r("perm_fold");
+    st = perm_fold_async(p, gather, world, d_out);
+  }
   if (st) return st;
   CUDA_TRY(cudaEventRecord(p->ev[3], p->stream));
   return PERM_OK;
