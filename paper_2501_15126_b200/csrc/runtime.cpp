@@ -334,8 +334,12 @@ int load_device_impl(perm_plan_s* p) {
   for (auto& ev : p->ev) CUDA_TRY(cudaEventCreate(&ev));
   lap("stream+events");
   CUDA_TRY(pool_alloc(p->device, &p->d_partial, p->partial_bytes));
+  // the result / partial slots are 16 bytes (complex, u128) and copied back
+  // whole; FP64 writes 8 of them: zero them once (compute-sanitizer initcheck)
+  CUDA_TRY(cudaMemsetAsync(p->d_partial, 0, p->partial_bytes, p->stream));
   p->scratch_bytes = 16 * 128;
   CUDA_TRY(pool_alloc(p->device, &p->d_scratch, p->scratch_bytes));
+  CUDA_TRY(cudaMemsetAsync(p->d_scratch, 0, p->scratch_bytes, p->stream));
   CUDA_TRY(pool_alloc(p->device, &p->d_counter, p->counter_bytes));
   if (!p->singular && !p->trivial1) {
     p->lib_key.assign(p->cubin.begin(), p->cubin.end());
@@ -748,7 +752,22 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
       }
     }
   }
-  if (!plan_hit) {
+  if (!plan_hit && p->singular) {
+    // structural rank < n: perm = 0 exactly with no kernel; nothing to
+    // order, eliminate or compile (an all-zero column would otherwise reach
+    // the ordering and the generator)
+    p->rowp.resize(n);
+    p->colp.resize(n);
+    for (int i = 0; i < n; ++i) {
+      p->rowp[i] = p->colp[i] = i;
+      I.row_perm[i] = I.col_perm[i] = i;
+    }
+    I.ordering = PERM_ORDER_NONE;
+    I.K = 0;
+    I.candidates_compiled = 0;
+    I.w_alg1 = 0;
+  }
+  if (!plan_hit && !p->singular) {
     const double tc = now_ms();
     // candidates: base ordering x K factored columns (greedy row-disjoint
     // picks in base order, DESIGN "Factored columns"); pick the lowest W_plan
@@ -1546,7 +1565,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
     if (g_plan_cache.size() > 256) g_plan_cache.clear();
     g_plan_cache[pkey] = *p;
   }
-  if (!plan_hit && !cache_file.empty()) {  // atomic publish: write a temp file, rename
+  if (!plan_hit && !p->singular && !cache_file.empty()) {  // atomic publish: write a temp file, rename
     const std::string blob = plan_serialize(*p, pkey);
     const std::string tmp = cache_file + ".tmp." + std::to_string((long long)getpid());
     if (FILE* f = fopen(tmp.c_str(), "wb")) {

@@ -408,3 +408,19 @@ def test_opts_world_validation_and_result_fields():
     assert P.info["B"] <= 4
     with pytest.raises(pb.PermError):   # no device: compute fails loudly (no CPU fallback)
         P.compute_ex()
+
+
+def test_empty_column_is_singular_without_planning():
+    """An all-zero column (or row) is structural rank < n: perm = 0 with no
+    ordering, codegen or kernel (this used to reach the generator)."""
+    A = synth.erdos_renyi(18, 0.3, 1)
+    for k in range(2):
+        S = A.copy()
+        if k == 0:
+            S[:, 5] = 0
+        else:
+            S[5, :] = 0
+        P = pb.Plan.from_dense(S, no_device=True)
+        assert P.info["singular"] == 1 and P.info["struct_rank"] == 17
+        assert P.info["row_perm"] == list(range(18)) and P.info["K"] == 0
+        P.close()

@@ -684,3 +684,15 @@ def test_int01_autotune_with_asm_candidate_bit_exact():
     B = synth.erdos_renyi(34, 0.2, 1, binary=True)
     P = plan(B, mode="int01", autotune=0)
     assert P.exact() == oracle.perm_nw_exact(B)
+
+
+def test_empty_column_exact_zero_every_mode():
+    A = synth.erdos_renyi(18, 0.3, 1)
+    S = A.copy()
+    S[:, 5] = 0
+    assert plan(S).compute() == 0.0
+    B = (S != 0).astype(float)
+    assert plan(B, mode="int01").exact() == 0
+    Z = S * (1 + 0.5j)
+    r = plan(Z).compute_ex()
+    assert r.value == 0.0 and r.value_im == 0.0
