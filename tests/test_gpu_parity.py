@@ -696,3 +696,33 @@ def test_empty_column_exact_zero_every_mode():
     Z = S * (1 + 0.5j)
     r = plan(Z).compute_ex()
     assert r.value == 0.0 and r.value_im == 0.0
+
+
+def test_random_shapes_fuzz_vs_oracle():
+    """Seeded fuzz over sizes 1-20, densities 0.05-1, signed values, 0/1
+    patterns, zero columns and diagonally dominated inputs, in every mode the
+    input admits: every permanent against the oracle (exact for INT01)."""
+    rng = np.random.default_rng(11)
+    checked = 0
+    for it in range(40):
+        n = int(rng.integers(1, 21))
+        p = float(rng.choice([0.05, 0.1, 0.2, 0.5, 1.0]))
+        A = (rng.random((n, n)) < p) * (rng.random((n, n)) * 2 - 1)
+        kind = int(rng.integers(0, 4))
+        if kind == 1:
+            A = (A != 0).astype(float)
+        if kind == 2 and n > 2:
+            A[:, int(rng.integers(0, n))] = 0
+        if kind == 3:
+            A = A + np.eye(n) * 0.5
+        exp, terms = oracle.perm_nw(A)
+        for mode in (["reg", "hybrid", "int01"] if kind == 1 else ["reg", "hybrid"]):
+            P = plan(A, mode=mode)
+            if mode == "int01":
+                assert P.exact() == oracle.perm_nw_exact(A), (it, n, p)
+            else:
+                v = P.compute()
+                assert abs(v - exp) <= 1e-9 * max(abs(exp), 1e-3 * terms, 1e-300), (it, n, p, kind, mode, v, exp)
+            P.close()
+            checked += 1
+    assert checked >= 80
