@@ -1537,20 +1537,40 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
     // U..B-1 are blk, bit B is chunk bit 0 (= lane bit 0); a 32-bit hu keeps
     // the 64-bit h0 out of the loop (registers)
     const std::string hu_init = "const unsigned cb = ((unsigned)lane & 1u) << " + std::to_string(B - U) + ";";
+    // software-pipelined dispatch (complex sweeps): the next block's flip j
+    // and sign (BREV/FLO/shifts, MIO latency) are computed before this
+    // block's body, and the most frequent flip (bit U, every other block) is
+    // a direct uniform branch instead of the switch's BRX.  Measured
+    // (profiles/r2_xform_variants_dispatch.jsonl): complex band n=44 +1.6 %;
+    // the real kernels gain nothing or spill, so they keep the plain switch.
+    const char* pd_env = getenv("PERM_PIPE_DISPATCH");
+    const bool pipe_dispatch = pd_env ? atoi(pd_env) == 1 : g.cx;
+    const std::string sty = g.i01 ? "int" : "double";
+    const std::string splus = g.i01 ? "2" : "1.0", sminus = g.i01 ? "-2" : "-1.0";
     if (nblk > 1) {
       g.line(hu_init);
+      if (pipe_dispatch) {
+        g.line("unsigned jn_ = " + std::to_string(U) + ";");
+        g.line("unsigned sb_ = ((cb | 1u) >> 1) & 1u;  // sign bit of the next block's flip");
+      }
       g.line("#pragma unroll 1");
       g.line("for (unsigned blk = 0; blk < " + std::to_string(nblk) + "u; ++blk) {");
       g.ind = "        ";
       g.line("const unsigned hu = cb | blk;");
       g.line("if (blk != 0) {");
       g.ind = "          ";
-      g.line("const int j = " + std::to_string(U - 1) + " + __ffs(blk);");
-      if (g.i01) g.line("const int s = ((hu >> (j + " + std::to_string(1 - U) + ")) & 1u) ? -2 : 2;");
-      else g.line("const double s = ((hu >> (j + " + std::to_string(1 - U) + ")) & 1u) ? -1.0 : 1.0;");
-      g.line("switch (j) {");
+      if (pipe_dispatch) {
+        g.line("const int j = (int)jn_;");
+        g.line("const " + sty + " s = sb_ ? " + sminus + " : " + splus + ";");
+      } else {
+        g.line("const int j = " + std::to_string(U - 1) + " + __ffs(blk);");
+        g.line("const " + sty + " s = ((hu >> (j + " + std::to_string(1 - U) + ")) & 1u) ? " + sminus + " : " + splus + ";");
+      }
+      if (!pipe_dispatch) g.line("switch (j) {");
       for (int b = U; b < B; ++b) {
-        g.line("case " + std::to_string(b) + ": {");
+        if (pipe_dispatch && b == U) g.line("if (blk & 1u) {  // bit U: every other block");
+        else if (pipe_dispatch && b == U + 1) g.line("} else switch (j) {");
+        if (!(pipe_dispatch && b == U)) g.line("case " + std::to_string(b) + ": {");
         std::string save = g.ind;
         g.ind += "  ";
         g.ops = 0;
@@ -1559,13 +1579,24 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
         g.flip(b, "s");
         g.end_region();
         ops_switch += g.ops * (double)(1ull << (B - 1 - b));  // flips of bit b per chunk
-        g.line("break; }");
+        if (!(pipe_dispatch && b == U)) g.line("break; }");
         g.ind = save;
       }
-      g.line("default: break;");
-      g.line("}");
+      if (pipe_dispatch && B == U + 1) {
+        g.line("}");  // bit U is the only block bit: no switch
+      } else {
+        g.line("default: break;");
+        g.line("}");
+      }
       g.ind = "        ";
       g.line("}");
+      if (pipe_dispatch) {
+        g.line("{");
+        g.line("  const unsigned b1_ = blk + 1u;");
+        g.line("  jn_ = " + std::to_string(U - 1) + " + __ffs(b1_ | (1u << 30));");
+        g.line("  sb_ = ((cb | b1_) >> (jn_ + " + std::to_string(1 - U) + ")) & 1u;");
+        g.line("}");
+      }
     } else {
       g.line(hu_init);
       g.line("{");

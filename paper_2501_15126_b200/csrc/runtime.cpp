@@ -694,7 +694,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
                           "PERM_PLAN_COMPILES", "PERM_NO_AUTOTUNE", "PERM_ALLOW_SPILL", "PERM_PLAN_BUDGET",
                           // codegen post-pass knobs (codegen.cpp post_pass)
                           "PERM_NO_SMEM", "PERM_SMEM_ALL", "PERM_NO_DCE", "PERM_NO_FUSE", "PERM_NO_KC", "PERM_KC_CAP", "PERM_SMEM_VOL_FRAC", "PERM_LADDER_RUNGS",
-                          "PERM_NO_ASM_MUL", "PERM_ASM_MUL"}) {
+                          "PERM_NO_ASM_MUL", "PERM_ASM_MUL", "PERM_PIPE_DISPATCH"}) {
       const char* v = getenv(k);
       pkey += k;
       pkey += '=';

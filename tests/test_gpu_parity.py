@@ -638,7 +638,8 @@ def test_reseed_interval_caps_the_chunk():
 # ---- codegen post-pass variants (DESIGN 3.13(d)/(e)) ---------------------------
 
 @pytest.mark.parametrize("env", [{"PERM_SMEM_VOL_FRAC": "1"}, {"PERM_SMEM_VOL_FRAC": "0"},
-                                 {"PERM_NO_KC": "1"}, {"PERM_SMEM_VOL_FRAC": "1", "PERM_KC_CAP": "8"}])
+                                 {"PERM_NO_KC": "1"}, {"PERM_SMEM_VOL_FRAC": "1", "PERM_KC_CAP": "8"},
+                                 {"PERM_PIPE_DISPATCH": "1"}, {"PERM_PIPE_DISPATCH": "0"}])
 def test_post_pass_variants_vs_oracle(env, monkeypatch):
     """Every shared-memory-slot flavour (all volatile, all plain; the complex
     volatile proxy) and the literal table on / off / small, in FP64, complex
