@@ -1010,7 +1010,8 @@ struct PostStats {
 //    needs (at n=40 29 of 68 loop-carried doubles qualify).
 PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, size_t nregions, bool fuse,
                     int body_region = -1, int threads = 128, bool hoist_lits = false,
-                    const std::vector<double>* region_weight = nullptr, double vol_frac_default = 0.5) {
+                    const std::vector<double>* region_weight = nullptr, double vol_frac_default = 0.5,
+                    bool w_only = false) {
   PostStats ps;
   ps.region_ops.assign(nregions, 0.0);
   auto tp = [](){ return std::chrono::steady_clock::now(); };
@@ -1018,7 +1019,8 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
     return (long long)std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count(); };
   const auto T0 = tp();
   struct Ln {
-    std::string text;
+    std::string_view text;      // the line: a view into src, or into own once rewritten
+    std::string own;
     int region = -1, kind = 0;  // 1 const def, 2 register decl, 3 register assign
     int name = -1;              // defined / assigned identifier
     std::vector<int> toks;      // identifier ids on the line (all occurrences)
@@ -1051,7 +1053,7 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
         continue;
       }
       Ln l;
-      l.text = std::string(s);
+      l.text = s;
       l.region = region;
       for (size_t i = 0; i < s.size();) {
         if (isid0(s[i]) && (i == 0 || !isid(s[i - 1]))) {
@@ -1139,21 +1141,30 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
       if (L[k].kind == 1) def_line[L[k].name] = (int)k;
     }
     const std::string pre = "const double ";
-    struct Bin { std::string a, op, b, indent; };
+    // "<indent>const double NAME = A op B;" with op one of * + - (views into the line)
+    struct Bin { std::string_view a, op, b, indent; };
     auto parse = [&](const Ln& l, Bin& b) {
-      const size_t p = l.text.find(pre);
-      if (p == std::string::npos || l.text.find_first_not_of(' ') != p) return false;
-      const size_t eq = l.text.find(" = ", p);
-      const std::string e = l.text.substr(eq + 3, l.text.size() - eq - 4);
-      std::istringstream es(e);
-      std::vector<std::string> tok;
-      std::string t;
-      while (es >> t) tok.push_back(t);
-      if (tok.size() != 3 || tok[1].size() != 1 || !std::strchr("*+-", tok[1][0])) return false;
-      b = {tok[0], tok[1], tok[2], l.text.substr(0, p)};
+      const std::string_view t(l.text);
+      const size_t p = t.find_first_not_of(' ');
+      if (p == std::string_view::npos || t.compare(p, pre.size(), pre) != 0) return false;
+      const size_t eq = t.find(" = ", p);
+      if (eq == std::string_view::npos || t.size() < eq + 4) return false;
+      const std::string_view e = t.substr(eq + 3, t.size() - eq - 4);
+      std::string_view tok[4];
+      int nt = 0;
+      for (size_t i = 0; i < e.size();) {
+        if (e[i] == ' ' || e[i] == '\t') { ++i; continue; }
+        size_t j = i;
+        while (j < e.size() && e[j] != ' ' && e[j] != '\t') ++j;
+        if (nt == 3) return false;
+        tok[nt++] = e.substr(i, j - i);
+        i = j;
+      }
+      if (nt != 3 || tok[1].size() != 1 || !std::strchr("*+-", tok[1][0])) return false;
+      b = {tok[0], tok[1], tok[2], t.substr(0, p)};
       return true;
     };
-    auto single_mul = [&](const std::string& v, int sgu, Bin& m) -> int {
+    auto single_mul = [&](std::string_view v, int sgu, Bin& m) -> int {
       auto it = ids.find(v);
       if (it == ids.end() || occ[it->second] != 2) return -1;
       auto d = def_line.find(it->second);
@@ -1165,14 +1176,17 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
       Ln& l = L[k];
       Bin c, m;
       if (!l.alive || l.kind != 1 || !parse(l, c) || c.op == "*") continue;
-      const std::string name = idname[l.name];
-      const std::string neg = c.op == "-" ? "-" : "";
+      const std::string& name = idname[l.name];
+      const char* neg = c.op == "-" ? "-" : "";
       int d = single_mul(c.a, seg[k], m);
       std::string text;
+      auto cat = [&text](std::initializer_list<std::string_view> parts) {
+        for (std::string_view v : parts) text.append(v.data(), v.size());
+      };
       if (d >= 0) {
-        text = c.indent + pre + name + " = fma(" + m.a + ", " + m.b + ", " + neg + c.b + ");";
+        cat({c.indent, pre, name, " = fma(", m.a, ", ", m.b, ", ", neg, c.b, ");"});
       } else if ((d = single_mul(c.b, seg[k], m)) >= 0) {
-        text = c.indent + pre + name + " = fma(" + neg + m.a + ", " + m.b + ", " + c.a + ");";
+        cat({c.indent, pre, name, " = fma(", neg, m.a, ", ", m.b, ", ", c.a, ");"});
       } else {
         continue;
       }
@@ -1186,15 +1200,16 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
           --occ[ta];
           break;
         }
-      for (const std::string* v : {&m.a, &m.b})
-        if (!v->empty() && isid0((*v)[0])) {
-          const int id = intern(*v);
+      for (std::string_view v : {m.a, m.b})
+        if (!v.empty() && isid0(v[0])) {
+          const int id = intern(v);
           if (id >= (int)occ.size()) occ.resize(id + 1, 0);
           l.toks.push_back(id);
           ++occ[id];
         }
       ++ps.fused;
-      l.text = text;
+      l.own = std::move(text);  // the views in c and m are not used past this point
+      l.text = l.own;
     }
   }
   const auto T3 = tp();
@@ -1229,7 +1244,7 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
     // struct has no assignment operator).
     const double vol_frac = getenv("PERM_SMEM_VOL_FRAC") ? atof(getenv("PERM_SMEM_VOL_FRAC")) : vol_frac_default;
     std::map<int, double> acc_w;  // value -> executions per chunk of the regions touching it (seed excluded)
-    if (region_weight)
+    if (region_weight && !w_only)  // only the volatile split reads it (not W or the registers)
       for (const Ln& l : L)
         if (l.alive && l.region > 0 && l.region != body_region && l.region < (int)region_weight->size())
           for (int t : std::set<int>(l.toks.begin(), l.toks.end())) acc_w[t] += (*region_weight)[l.region];
@@ -1266,19 +1281,19 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
   }
   auto rename = [&](Ln& l) {  // moved names -> SM_name (declarations become stores)
     std::string t;
-    const std::string& s0 = l.text;
+    const std::string_view s0 = l.text;
     size_t i = 0;
     if (l.kind == 2 && moved.count(l.name)) {  // "  TYPE name = expr;" -> "  SM_name = expr;"
       const size_t p0 = s0.find_first_not_of(' ');
       const size_t p1 = s0.find(idname[l.name], p0);
-      t = s0.substr(0, p0);
+      t = std::string(s0.substr(0, p0));
       i = p1;
     }
     while (i < s0.size()) {
       if (isid0(s0[i]) && (i == 0 || !isid(s0[i - 1]))) {
         size_t j = i;
         while (j < s0.size() && isid(s0[j])) ++j;
-        const std::string w = s0.substr(i, j - i);
+        const std::string w(s0.substr(i, j - i));
         auto it = ids.find(w);
         if (it != ids.end() && moved.count(it->second)) t += "SM_";
         t += w;
@@ -1287,7 +1302,8 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
         t += s0[i++];
       }
     }
-    l.text = t;
+    l.own = std::move(t);
+    l.text = l.own;
   };
   // ---- 5. hot literals -> __constant__ table.  sm_100a FP64 instructions
   // take no constant-bank operand: a literal becomes a uniform register
@@ -1301,7 +1317,7 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
   std::string kc_decl;
   std::unordered_map<std::string, int> kc_index;
   if (hoist_lits && body_region >= 0 && !getenv("PERM_NO_KC")) {
-    auto lit_at = [](const std::string& t, size_t i, size_t& a, size_t& e) {  // "(0x..p..)" / "(-0x..p..)"
+    auto lit_at = [](std::string_view t, size_t i, size_t& a, size_t& e) {  // "(0x..p..)" / "(-0x..p..)"
       if (t[i] != '(') return false;
       size_t j = i + 1;
       if (j < t.size() && t[j] == '-') ++j;
@@ -1322,7 +1338,7 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
       if (l.alive && l.region == body_region)
         for (size_t i = 0, a, e; i < l.text.size(); ++i)
           if (lit_at(l.text, i, a, e)) {
-            ++cnt[l.text.substr(a, e - a)];
+            ++cnt[std::string(l.text.substr(a, e - a))];
             i = e;
           }
     std::vector<std::pair<int, std::string>> hot;
@@ -1346,10 +1362,10 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
         bool any = false;
         for (size_t i = 0, a, e; i < l.text.size(); ++i) {
           if (lit_at(l.text, i, a, e)) {
-            auto it = kc_index.find(l.text.substr(a, e - a));
+            auto it = kc_index.find(std::string(l.text.substr(a, e - a)));
             if (it != kc_index.end()) {
               t += '(';
-              t.append(l.text, i + 1, a - i - 1);  // sign
+              t.append(l.text.data() + i + 1, a - i - 1);  // sign
               t += "kc_[" + std::to_string(it->second) + "])";
               i = e;
               any = true;
@@ -1358,10 +1374,28 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
           }
           t += l.text[i];
         }
-        if (any) l.text.swap(t);
+        if (any) {
+          l.own = std::move(t);
+          l.text = l.own;
+        }
       }
       ps.hoisted = (int)hot.size();
     }
+  }
+  if (w_only) {  // planner scoring: the per-region counts and registers, no source text
+    for (const Ln& l : L) {
+      if (!l.alive) continue;
+      if (l.kind == 1 && l.region >= 0 && l.region < (int)nregions) {
+        auto it = wt.find(idname[l.name]);
+        if (it != wt.end()) ps.region_ops[l.region] += it->second;
+      }
+      if (l.kind == 2 && !moved.count(l.name)) {
+        const std::string& ty = idname[l.toks[0]];
+        ps.reg_words += ty == "int" ? 1 : ((ty == "double" || ty == "i64") ? 2 : 4);
+      }
+    }
+    g_pp_ns[3] += ns(T3, tp());
+    return ps;
   }
   std::string out;
   out.reserve(src.size() + smem_decl.size() + kc_decl.size());
@@ -1658,7 +1692,7 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
                                    !g.i01 && !S.w_only, &g.region_weight,
                                    // measured on B200 (profiles/r2_smem_vol_ab.txt): real FP64 0.5,
                                    // INT01 0.125, complex 0 (its 3-block volatile kernels run slower)
-                                   g.cx ? 0.0 : (g.i01 ? 0.125 : 0.5));
+                                   g.cx ? 0.0 : (g.i01 ? 0.125 : 0.5), S.w_only);
   g_post_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_post0).count();
   kc.smem_bytes = ps.smem_bytes;
   double chunk_ops = 1.0;  // + lacc
