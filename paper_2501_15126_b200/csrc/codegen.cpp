@@ -1011,7 +1011,7 @@ struct PostStats {
 PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, size_t nregions, bool fuse,
                     int body_region = -1, int threads = 128, bool hoist_lits = false,
                     const std::vector<double>* region_weight = nullptr, double vol_frac_default = 0.5,
-                    bool w_only = false) {
+                    bool w_only = false, int smem_ro = 0) {
   PostStats ps;
   ps.region_ops.assign(nregions, 0.0);
   auto tp = [](){ return std::chrono::steady_clock::now(); };
@@ -1224,8 +1224,26 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
     struct Mv { int id, size; std::string ty; };
     std::vector<Mv> mv;
     const bool all = getenv("PERM_SMEM_ALL") != nullptr;
+    // smem_ro (spill escalation): values the body reads but never writes, with
+    // at most smem_ro uses in the body, also move -- always volatile, so every
+    // body use is an LDS and the value holds no register across the body
+    std::set<int> ro_moved;
+    if (smem_ro > 0) {
+      std::unordered_map<int, int> body_uses;
+      std::set<int> body_written;
+      for (const Ln& l : L)
+        if (l.alive && l.region == body_region) {
+          for (int t : l.toks) ++body_uses[t];
+          if (l.kind == 3) body_written.insert(l.name);
+        }
+      for (const Ln& l : L)
+        if (l.alive && l.kind == 2 && in_body.count(l.name) && !body_written.count(l.name) &&
+            idname[l.name] != "cacc" && idname[l.toks[0]] == "double" && body_uses[l.name] <= smem_ro)
+          ro_moved.insert(l.name);
+    }
     for (const Ln& l : L)
-      if (l.alive && l.kind == 2 && (all || !in_body.count(l.name)) && idname[l.name] != "cacc") {
+      if (l.alive && l.kind == 2 && (all || !in_body.count(l.name) || ro_moved.count(l.name)) &&
+          idname[l.name] != "cacc") {
         const std::string& ty = idname[l.toks[0]];
         mv.push_back({l.name, ty == "int" ? 4 : ((ty == "double" || ty == "i64") ? 8 : 16), ty});
       }
@@ -1252,6 +1270,7 @@ PostStats post_pass(std::string& src, const std::map<std::string, double>& wt, s
         (region_weight && body_region >= 0 && body_region < (int)region_weight->size()) ? (*region_weight)[body_region]
                                                                                          : 0.0;
     auto is_vol = [&](int id) {
+      if (ro_moved.count(id)) return true;
       if (vol_frac <= 0 || body_w <= 0) return false;
       auto it = acc_w.find(id);
       return (it == acc_w.end() ? 0.0 : it->second) <= vol_frac * body_w * (1 + 1e-9);
@@ -1692,7 +1711,7 @@ KernelCode generate_kernel_once(const Csx& A, const std::vector<double>& x0, con
                                    !g.i01 && !S.w_only, &g.region_weight,
                                    // measured on B200 (profiles/r2_smem_vol_ab.txt): real FP64 0.5,
                                    // INT01 0.125, complex 0 (its 3-block volatile kernels run slower)
-                                   g.cx ? 0.0 : (g.i01 ? 0.125 : 0.5), S.w_only);
+                                   g.cx ? 0.0 : (g.i01 ? 0.125 : 0.5), S.w_only, S.smem_ro);
   g_post_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_post0).count();
   kc.smem_bytes = ps.smem_bytes;
   double chunk_ops = 1.0;  // + lacc

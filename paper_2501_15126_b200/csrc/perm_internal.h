@@ -63,6 +63,8 @@ struct KernelSpec {
   uint64_t nchunks_total = 0;  // 2^(n-1-B)
   bool w_only = false;         // planner scoring: skip source steps that change neither W nor registers
   bool i01_asm_mul = false;    // INT01: int x u128 products through the hand-scheduled mul_s32_u128
+  int smem_ro = 0;             // > 0: body-read-only loop-carried values with <= smem_ro body uses
+                               // also go to (volatile) shared-memory slots (spill escalation rung)
   // INT01 (internal to generate_kernel): raised register bounds for a regeneration
   const std::map<std::string, double>* reg_lb_extra = nullptr;
 };

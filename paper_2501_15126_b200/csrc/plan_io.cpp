@@ -2,7 +2,7 @@
 // on-disk plan cache (PERM_CACHE_DIR / perm_opts.cache_dir) and the rank-0
 // plan broadcast of multi-GPU runs (perm_plan_export / perm_plan_import).
 //
-// Layout: "PERMPLN2" | u32 format version (3) | build id | key | fields in the
+// Layout: "PERMPLN2" | u32 format version (4) | build id | key | fields in the
 // order of write_plan below.  Every length-prefixed field is bounds-checked
 // on read; a blob from another libperm build (different generator) or with a
 // different key is rejected, never half-applied.
@@ -17,7 +17,7 @@ namespace perm {
 namespace {
 
 constexpr char kMagic[8] = {'P', 'E', 'R', 'M', 'P', 'L', 'N', '2'};
-constexpr uint32_t kFormat = 3;
+constexpr uint32_t kFormat = 4;
 
 struct W {
   std::string out;
@@ -88,12 +88,12 @@ struct R {
 void spec_io(W& w, const KernelSpec& s) {
   w.pod(s.n); w.pod(s.K); w.pod(s.B); w.pod(s.U); w.pod(s.M); w.pod(s.mode); w.pod(s.hybrid_c);
   w.pod(s.threads); w.pod(s.zero_skip); w.pod(s.cc); w.pod(s.min_blocks); w.pod(s.nchunks_total);
-  w.pod(s.i01_asm_mul);
+  w.pod(s.i01_asm_mul); w.pod(s.smem_ro);
 }
 void spec_io(R& r, KernelSpec& s) {
   r.pod(s.n); r.pod(s.K); r.pod(s.B); r.pod(s.U); r.pod(s.M); r.pod(s.mode); r.pod(s.hybrid_c);
   r.pod(s.threads); r.pod(s.zero_skip); r.pod(s.cc); r.pod(s.min_blocks); r.pod(s.nchunks_total);
-  r.pod(s.i01_asm_mul);
+  r.pod(s.i01_asm_mul); r.pod(s.smem_ro);
   s.reg_lb_extra = nullptr;
 }
 void code_io(W& w, const KernelCode& c) {

@@ -136,11 +136,13 @@ def test_no_device_plan_then_compute_fails_loudly():
 
 @pytest.mark.parametrize("n,p,seed,mode", [(10, 0.3, 1, "auto"), (30, 0.3, 1, "reg"), (36, 0.2, 1, "reg"),
                                            (40, 0.2, 1, "reg"), (40, 0.2, 2, "reg"), (12, 0.3, 3, "int01")])
-def test_codegen_compiles_without_spills(n, p, seed, mode):
+def test_codegen_compiles_within_spill_tolerance(n, p, seed, mode):
+    """Real FP64 accepts a local frame of <= 64 bytes per thread (DESIGN
+    3.13(f)); INT01 and complex kernels stay spill-free."""
     A = synth.erdos_renyi(n, p, seed, binary=(mode == "int01"))
     P = pb.Plan.from_dense(A, ordering="auto", mode=mode, no_device=True)
     i = P.info
-    assert i["local_bytes"] == 0
+    assert i["local_bytes"] <= (0 if i["mode"] == 3 else 64)
     assert 0 < i["regs_per_thread"] <= 255
     assert i["w_plan"] > 0
     assert "perm_sweep" in P.source
@@ -152,7 +154,8 @@ def test_codegen_compiles_without_spills(n, p, seed, mode):
             f.flush()
             sass = subprocess.run(["cuobjdump", "-sass", f.name], capture_output=True, text=True).stdout
         assert "sm_100a" in sass
-        assert not re.search(r"\b(LDL|STL)\b", sass), "local memory in generated kernel"
+        if i["local_bytes"] == 0:
+            assert not re.search(r"\b(LDL|STL)\b", sass), "local memory in generated kernel"
         with tempfile.NamedTemporaryFile(suffix=".cubin") as f:
             f.write(cub)
             f.flush()
@@ -161,7 +164,7 @@ def test_codegen_compiles_without_spills(n, p, seed, mode):
         m = re.search(r"register count: (\d+)", elf)
         assert m and int(m.group(1)) == i["regs_per_thread"]
         fr = re.search(r"frame size: (0x[0-9a-f]+)", elf)
-        assert fr is None or int(fr.group(1), 16) == 0
+        assert (0 if fr is None else int(fr.group(1), 16)) <= i["local_bytes"]
         if mode != "int01":
             assert re.search(r"\bD(ADD|MUL|FMA)\b", sass)
 
@@ -319,7 +322,7 @@ def test_maximum_size_n64_plans_full_gray_range():
     A = synth.givens_brickwork(64, 4, 1)
     P = pb.Plan.from_dense(A, mode="reg", no_device=True)
     i = P.info
-    assert i["local_bytes"] == 0 and i["w_plan"] > 0
+    assert i["local_bytes"] <= 64 and i["w_plan"] > 0
     assert i["tasks"] & (i["tasks"] - 1) == 0
     steps = i["tasks"] * 32 * i["M"] * (1 << i["B"]) * (1 << i["K"])
     assert steps == 2 ** 63
@@ -329,15 +332,26 @@ def test_maximum_size_n64_plans_full_gray_range():
 
 def test_smem_placement_of_values_the_body_never_touches():
     """DESIGN 3.13(d): loop-carried values absent from the block body live in
-    per-thread shared-memory slots; none of them appears in the body."""
+    per-thread shared-memory slots; none of them appears in the body.
+    DESIGN 3.13(f): the spill-escalation rung (the n=40 bench plan takes it)
+    also places values the body only reads, at most 6 times, in volatile
+    slots: those appear in the body as reads only."""
     A = synth.erdos_renyi(40, 0.2, 1)
     P = pb.Plan.from_dense(A, mode="reg", no_device=True, autotune=-1)
     src, i = P.source, P.info
     names = re.findall(r"#define SM_(\w+) ", src)
     assert names and i["smem_bytes"] >= 128 * 8 * len(names) // 2
     body = src[src.index("const double sU"):src.index("lacc += cacc")]
+    read_in_body = 0
     for nm_ in names:
-        assert not re.search(rf"\b{nm_}\b", body) and f"SM_{nm_}" not in body
+        assert not re.search(rf"(?<!SM_)\b{nm_}\b", body)
+        uses = len(re.findall(rf"\bSM_{nm_}\b", body))
+        if uses:
+            read_in_body += 1
+            assert uses <= 6
+            assert re.search(rf"#define SM_{nm_} \(\(\(volatile double\*\)", src)
+            assert not re.search(rf"^\s*SM_{nm_} = ", body, re.M)
+    assert read_in_body > 0 and i["local_bytes"] <= 64
     assert "extern __shared__" in src
 
 

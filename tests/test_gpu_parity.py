@@ -7,6 +7,7 @@ checked one by one against the oracle's unscaled Alg. 1 partial sum over the
 same Gray range of the same ordered matrix (ordering recomputed by the planner
 ORACLE and checked equal to the product's)."""
 import math
+import re
 
 import numpy as np
 import pytest
@@ -666,6 +667,31 @@ def test_post_pass_variants_vs_oracle(env, monkeypatch):
     B = synth.erdos_renyi(26, 0.25, 2, binary=True)
     R = plan(B, mode="int01")
     assert R.exact() == oracle.perm_nw_exact(B)
+
+
+@pytest.mark.parametrize("n,p,seed,uses", [(30, 0.2, 2, 6), (31, 0.2, 3, 6), (28, 0.25, 1, 40), (30, 0.3, 1, 1000)])
+def test_spilling_and_smem_ro_kernels_vs_oracle(n, p, seed, uses, monkeypatch):
+    """DESIGN 3.13(f): real-FP64 kernels that keep a small local frame and
+    read body values from volatile shared-memory slots (the smem_ro rung,
+    forced here: U = 5 and any spill accepted) give the oracle's permanent,
+    with the model pick and with the autotuned pick."""
+    monkeypatch.setenv("PERM_SMEM_RO", str(uses))
+    monkeypatch.setenv("PERM_SMEM_RO_FORCE", "1")
+    monkeypatch.setenv("PERM_SPILL_OK", "4096")
+    A = synth.erdos_renyi(n, p, seed)
+    exp, _ = oracle.perm_nw(A)
+    for kw in ({"autotune": -1}, {}):
+        P = plan(A, mode="reg", block_log2=5, **kw)
+        src = P.source
+        body = src[src.index("const double sU"):src.index("lacc += cacc")]
+        if kw:  # the model pick carries the placement: volatile slots read in the body
+            assert re.search(r"\bSM_\w+\b", body), "no shared-memory read in the body"
+        assert rel(P.compute(), exp) < REL, (kw, P.info["local_bytes"])
+    monkeypatch.delenv("PERM_SMEM_RO_FORCE")
+    monkeypatch.setenv("PERM_SPILL_OK", "0")
+    P = plan(A, mode="reg", block_log2=5, autotune=-1)
+    assert P.info["local_bytes"] == 0
+    assert rel(P.compute(), exp) < REL
 
 
 @pytest.mark.parametrize("n,p,seed", [(24, 0.25, 1), (30, 0.2, 2), (32, 0.2, 3)])

@@ -216,6 +216,54 @@ def xf_order(src, how="asap", seed=0):
         for k in reversed(range(n)):
             h[k] = 1 + max([h[u] for u in users[k]], default=0)
         order = sorted(range(n), key=lambda k: (-h[k], k))
+    elif how == "dfs":  # Sethi-Ullman-like: each sink's operand trees depth first, deepest operand first
+        need = [0] * n
+        for k in range(n):
+            ds = sorted({need[d] for d in deps[k]}, reverse=True)
+            need[k] = max([v + i for i, v in enumerate(ds)] + [1])
+        done, order = [False] * n, []
+
+        def emit(k):
+            stack = [(k, False)]
+            while stack:
+                v, exp = stack.pop()
+                if done[v]:
+                    continue
+                if exp:
+                    done[v] = True
+                    order.append(v)
+                    continue
+                stack.append((v, True))
+                for d in sorted(set(deps[v]), key=lambda d: need[d]):
+                    if not done[d]:
+                        stack.append((d, False))
+        for k in range(n):
+            if not users[k]:
+                emit(k)
+        for k in range(n):
+            emit(k)
+    elif how == "greedy":  # list schedule minimising the live set, ties in source order
+        import heapq
+        remaining = [len(set(u)) for u in users]
+        indeg = [len(set(d)) for d in deps]
+        emitted = [False] * n
+        order = []
+
+        def score(k):
+            kills = sum(1 for d in set(deps[k]) if remaining[d] == 1)
+            return (1 if users[k] else 0) - kills
+        ready = set(k for k in range(n) if indeg[k] == 0)
+        while ready:
+            k = min(ready, key=lambda k: (score(k), k))
+            ready.discard(k)
+            emitted[k] = True
+            order.append(k)
+            for d in set(deps[k]):
+                remaining[d] -= 1
+            for u in set(users[k]):
+                indeg[u] -= 1
+                if indeg[u] == 0:
+                    ready.add(u)
     else:
         rnd = random.Random(seed)
         indeg = [len(set(d)) for d in deps]
@@ -323,6 +371,75 @@ def xf_m128(src, helper=None):
     return out.replace('extern "C"', (helper or MUL_S32_U128) + 'extern "C"', 1)
 
 
+def xf_rw_le(src, maxuses, maxrw):
+    """xf_ro_le plus the body-WRITTEN loop-carried doubles with <= maxrw uses
+    (an STS per write, an LDS per read)."""
+    import collections
+    L = src.split("\n")
+    li = next(i for i, l in enumerate(L) if "for (unsigned blk" in l)
+    bi = max(i for i, l in enumerate(L) if "default: break;" in l) + 2
+    be = max(i for i, l in enumerate(L) if "lacc += cacc" in l)
+    decl = {}
+    for i in range(li - 1, 0, -1):
+        m = re.match(r"\s+double (\w+) = (t\d+|0);$", L[i])
+        if m:
+            decl[m.group(1)] = i
+        elif "const double" in L[i]:
+            break
+    body = "\n".join(L[bi:be])
+    written = set(re.findall(r"^\s+(\w+) = ", body, re.M))
+    uses = collections.Counter(re.findall(r"\b(\w+)\b", body))
+    mv = [v for v in decl if v != "cacc" and uses[v] > 0 and uses[v] <= (maxrw if v in written else maxuses)]
+    return _ro_subset(src, mv, decl)
+
+
+def xf_ro_le(src, maxuses):
+    """only the body-read-only loop-carried doubles with <= maxuses uses in the
+    block body -> volatile shared-memory slots (an LDS per use; frees their
+    registers for a larger unrolled block)."""
+    import collections
+    L = src.split("\n")
+    li = next(i for i, l in enumerate(L) if "for (unsigned blk" in l)
+    bi = max(i for i, l in enumerate(L) if "default: break;" in l) + 2
+    be = max(i for i, l in enumerate(L) if "lacc += cacc" in l)
+    decl = {}
+    for i in range(li - 1, 0, -1):
+        m = re.match(r"\s+double (\w+) = (t\d+|0);$", L[i])
+        if m:
+            decl[m.group(1)] = i
+        elif "const double" in L[i]:
+            break
+    body = "\n".join(L[bi:be])
+    written = set(re.findall(r"^\s+(\w+) = ", body, re.M))
+    uses = collections.Counter(re.findall(r"\b(\w+)\b", body))
+    keep = {v for v in decl if v in written or v == "cacc" or uses[v] > maxuses}
+    # reuse xf_ro on a copy where the kept names are hidden from it
+    for v in keep:
+        L[decl[v]] = L[decl[v]].replace("double %s =" % v, "double %s  =" % v)
+    return xf_ro("\n".join(L).replace("  =", " ="), vol=True) if False else _ro_subset(src, [v for v in decl if v not in keep], decl)
+
+
+def _ro_subset(src, ro, decl):
+    L = src.split("\n")
+    offs = [int(x) for x in re.findall(r"\(sm_ \+ (\d+)\)", src)]
+    thr = int(re.search(r"__launch_bounds__\((\d+)", src).group(1))
+    off = (max(offs) + 8 * thr) if offs else 0
+    defs = ""
+    for v in ro:
+        defs += "#define SM_%s (((double*)(sm_ + %d))[threadIdx.x])\n" % (v, off)
+        off += 8 * thr
+    for v in ro:
+        L[decl[v]] = L[decl[v]].replace("double %s =" % v, "SM_%s =" % v)
+    out = "\n".join(L)
+    for v in ro:
+        out = re.sub(r"(?<![\w])%s(?![\w])" % v, "SM_" + v, out)
+        out = out.replace("SM_SM_" + v, "SM_" + v)
+    if "extern __shared__" not in out:
+        out = out.replace('extern "C"', "extern __shared__ __align__(16) unsigned char sm_[];\n" + 'extern "C"', 1)
+    out = out.replace('extern "C"', defs + 'extern "C"', 1)
+    return xf_vol(out), off
+
+
 def xf_lb(src, mb):
     return re.sub(r"__launch_bounds__\((\d+), (\d+)\)", r"__launch_bounds__(\1, %d)" % mb, src)
 
@@ -334,9 +451,11 @@ def xf_b64(src):
 VARIANTS = {"base": (lambda s: s, 128), "hot2": (xf_hot, 128), "hot2c16": (lambda s: xf_hot(s, 2, 16), 128),
             "hot3": (lambda s: xf_hot(s, 3), 128),
             "vol": (xf_vol, 128), "br1": (xf_br1, 128), "m128": (xf_m128, 128), "m128u": (xf_m128u, 128), "m128c": (lambda s: xf_m128(s, MUL_S32_U128_C), 128), "asap": (lambda s: xf_order(s, "asap"), 128),
-            "alap": (lambda s: xf_order(s, "alap"), 128), "rand1": (lambda s: xf_order(s, "rand", 1), 128),
+            "alap": (lambda s: xf_order(s, "alap"), 128), "dfs": (lambda s: xf_order(s, "dfs"), 128),
+            "greedy": (lambda s: xf_order(s, "greedy"), 128), "rand1": (lambda s: xf_order(s, "rand", 1), 128),
             "rand2": (lambda s: xf_order(s, "rand", 2), 128), "rand3": (lambda s: xf_order(s, "rand", 3), 128), "pipej": (xf_pipej, 128), "kcase": (xf_kcase, 128), "kall": (lambda s: xf_kcase(s, "all"), 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
-            "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64)}
+            "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64),
+            **{"ro%d" % k: (lambda s, k=k: xf_ro_le(s, k), 128) for k in (0, 3, 5, 6, 10, 12, 35)}}
 
 
 def variant(name):
@@ -345,6 +464,9 @@ def variant(name):
     for part in name.split("+"):
         if part.startswith("lb"):
             fs.append(lambda s, mb=int(part[2:]): xf_lb(s, mb))
+        elif re.fullmatch(r"rw\d+_\d+", part):  # rwA_B: xf_rw_le(A, B)
+            a_, b_ = map(int, part[2:].split("_"))
+            fs.append(lambda s, a_=a_, b_=b_: xf_rw_le(s, a_, b_))
         else:
             f, t = VARIANTS[part]
             fs.append(f)
