@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libperm.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
-SOURCES = ["matrix.cpp", "codegen.cpp", "runtime.cpp", "plan_io.cpp", "collective.cpp", "reduce.cu", "probe.cu"]
+SOURCES = ["matrix.cpp", "codegen.cpp", "planner.cpp", "runtime.cpp", "plan_io.cpp", "collective.cpp", "reduce.cu", "probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -24,7 +24,7 @@ def _stale() -> bool:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, s) for s in SOURCES] + [
-        os.path.join(CSRC, "perm_internal.h"), os.path.join(CSRC, "plan_state.h"), os.path.join(ROOT, "include", "perm.h"), __file__]
+        os.path.join(CSRC, "perm_internal.h"), os.path.join(CSRC, "plan_state.h"), os.path.join(CSRC, "rt_internal.h"), os.path.join(ROOT, "include", "perm.h"), __file__]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
