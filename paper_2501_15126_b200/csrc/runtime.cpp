@@ -3,7 +3,6 @@
 // The kernel planner (searches, codegen candidates, NVRTC, autotune) is in
 // planner.cpp.  See include/perm.h.
 #include <cuda_runtime.h>
-#include <nvrtc.h>
 
 #include <algorithm>
 #include <atomic>
@@ -15,10 +14,8 @@
 #include <future>
 #include <map>
 #include <memory>
-#include <condition_variable>
 #include <mutex>
 #include <set>
-#include <thread>
 #include <string>
 #include <vector>
 

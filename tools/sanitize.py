@@ -4,8 +4,9 @@
     compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize.py
 
 FP64 plain sweep and column-eliminated sweep, the HYBRID global tier, INT01
-(block / warp-task zero skip), complex, a 2-shard fold, and a structurally
-singular input (no launch).  Each result is checked against the oracle."""
+(block / warp-task zero skip), complex, a 2-shard fold, spilling FP64 (with
+volatile shared-memory body reads) and INT01 kernels, a shard of the bench
+plan, and a structurally singular input (no launch).  Each result is checked against the oracle."""
 from __future__ import annotations
 
 import os
@@ -47,6 +48,29 @@ def main():
     ez = oracle.perm_band_complex(Z, synth.half_bandwidth(Z))
     assert abs(complex(r.value, r.value_im) - ez) <= 1e-9 * abs(ez)
     print("ok complex", flush=True)
+    # DESIGN 3.13(f): a spilling FP64 kernel that reads body values from
+    # volatile shared-memory slots (the smem_ro rung, forced), and a spilling
+    # INT01 kernel (accepted under autotune in production)
+    os.environ.update(PERM_SMEM_RO_FORCE="1", PERM_SPILL_OK="4096")
+    C = synth.erdos_renyi(22, 0.3, 2)
+    P = pb.Plan.from_dense(C, mode="reg", block_log2=5, autotune=-1)
+    assert P.info["local_bytes"] > 0 and "volatile double" in P.source
+    assert rel(P.compute(), oracle.perm_nw(C)[0]) < 1e-9
+    print("ok fp64 spill + smem_ro", P.info["local_bytes"], flush=True)
+    del os.environ["PERM_SMEM_RO_FORCE"]
+    os.environ["PERM_SPILL_OK"] = "64"
+    D = synth.erdos_renyi(26, 0.25, 3, binary=True)
+    Q = pb.Plan.from_dense(D, mode="int01", block_log2=4, autotune=-1)
+    assert Q.info["local_bytes"] > 0
+    assert Q.exact() == oracle.perm_nw_exact(D)
+    print("ok int01 spill", Q.info["local_bytes"], flush=True)
+    del os.environ["PERM_SPILL_OK"]
+    # the bench plan (n=40, K=8 B=8 U=5, 48-byte frame): one 1/128 shard
+    E = synth.erdos_renyi(40, 0.2, 1)
+    P = pb.Plan.from_dense(E, mode="reg", autotune=-1)
+    r = P.shard(0, 128)
+    assert r.value == r.value  # not NaN: the partial is checked against the oracle in tests/
+    print("ok bench plan shard", P.info["K"], P.info["U"], P.info["local_bytes"], flush=True)
     S = A.copy()
     S[:, 3] = 0
     S[:, 5] = 0
