@@ -744,7 +744,7 @@ Built Planner::build(const Cand& c) {
   std::vector<int> cp;
   order_with(c.base, b.rp, cp);
   b.tasks = geometry(c.K, b.sp, c.bcap);
-  b.colp = colp_of(cp, elim_of_base[c.base * 32 + c.ev], c.K, c.var, b.sp.B, nullptr, b.sp.U);
+  b.colp = colp_of(cp, elim_of_base.at(c.base * 32 + c.ev), c.K, c.var, b.sp.B, nullptr, b.sp.U);
   b.o = permute_ccs(p->ccs, b.rp, b.colp);
   b.xo = make_x0(b.o);
   b.sp.cc = c.cc;

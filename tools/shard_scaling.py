@@ -20,7 +20,7 @@ def main():
     ap.add_argument("--worlds", default="2,4,8")
     a = ap.parse_args()
     A = synth.erdos_renyi(a.n, a.p, a.seed)
-    P = pb.Plan.from_dense(A)
+    P = pb.Plan.from_dense(A, autotune=-1)  # the bench's model pick
     P.compute()
     t1 = min(P.compute_ex().sweep_ms for _ in range(3))
     full = P.compute()
