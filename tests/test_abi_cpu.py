@@ -373,6 +373,22 @@ def test_plan_export_import_roundtrip_no_device():
         pb.Plan.from_blob(b"X" + blob[1:], no_device=True)    # foreign magic
 
 
+def test_plan_export_import_keeps_spilling_smem_ro_kernel(monkeypatch):
+    """Plan format 4 (DESIGN 3.13(f)): a plan whose kernel keeps a local frame
+    and reads body values from volatile shared-memory slots travels through
+    export / import (rank-0 broadcast, disk cache) unchanged, and reports its
+    frame in local_bytes."""
+    monkeypatch.setenv("PERM_SMEM_RO_FORCE", "1")
+    monkeypatch.setenv("PERM_SPILL_OK", "4096")
+    A = synth.erdos_renyi(22, 0.3, 2)
+    P = pb.Plan.from_dense(A, mode="reg", block_log2=5, no_device=True, autotune=-1)
+    assert P.info["local_bytes"] > 0 and "volatile double" in P.source
+    Q = pb.Plan.from_blob(P.export(), no_device=True)
+    assert Q.source == P.source and Q.cubin() == P.cubin()
+    for k in ("K", "B", "U", "M", "tasks", "w_plan", "smem_bytes", "local_bytes", "regs_per_thread"):
+        assert Q.info[k] == P.info[k], k
+
+
 def test_disk_plan_cache(tmp_path):
     A = synth.erdos_renyi(22, 0.3, 5)
     d = str(tmp_path)
