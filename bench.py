@@ -558,7 +558,7 @@ def main():
                        "mode": ["auto", "reg", "hybrid", "int01"][info["mode"]],
                        "B": info["B"], "U": info["U"], "M": info["M"], "tasks": info["tasks"],
                        "k": info["k"], "c": info["c"],
-                       "regs": info["regs_per_thread"], "grid": info["grid"], "block": info["block"],
+                       "regs": info["regs_per_thread"], "local_bytes": info["local_bytes"], "smem_bytes": info["smem_bytes"], "grid": info["grid"], "block": info["block"],
                        "w_plan_fp64_ops_per_step": info["w_plan"], "w_alg1_ops_per_step": info["w_alg1"],
                        "K": info["K"], "plan_choice": "autotune" if kw["autotune"] == 0 else "model",
                        "plan_source": "rank 0 planned, blob broadcast to the other ranks" if world > 1 else "planned"},
