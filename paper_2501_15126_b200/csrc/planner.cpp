@@ -299,6 +299,8 @@ class Planner {
   int elim_maxsize = 96, elim_maxsize_big = 160, elim_maxsize_huge = 256;
   int elim_beam = 4;
   bool dbg_plan = false;
+  int task_bits = 17;            // floor of the warp-task count, log2 (geometry)
+  int score_b = 8;               // chunk-bit cap the elimination searches score at
 
   // ---- state shared by the phases
   // ev % 3: how the search scores a sequence -- 0: the kernel as planned
@@ -353,6 +355,8 @@ Planner::Planner(perm_plan_s* plan, perm_ordering ord_, double gr_, const std::s
   // beam width of the elimination searches (FP64: 4, INT01 / complex: greedy)
   elim_beam = std::max(1, getenv("PERM_ELIM_BEAM") ? atoi(getenv("PERM_ELIM_BEAM")) : (cplx_mode ? 1 : 4));
   dbg_plan = getenv("PERM_DEBUG_PLAN") != nullptr;
+  task_bits = getenv("PERM_TASK_BITS") ? atoi(getenv("PERM_TASK_BITS")) : 17;
+  score_b = getenv("PERM_SCORE_B") ? atoi(getenv("PERM_SCORE_B")) : 8;
 }
 
 int Planner::run() {
@@ -367,7 +371,6 @@ uint64_t Planner::geometry(int K, KernelSpec& sp, int bcap) const {
   const int nb = std::max(0, n - 1 - K);  // h-bits
   // at least 2^17 warp-tasks when the range allows (B >= 8): >= 14 tasks per
   // resident warp on each of 8 GPUs keeps the dynamic-scheduling tail small
-  static const int task_bits = getenv("PERM_TASK_BITS") ? atoi(getenv("PERM_TASK_BITS")) : 17;
   const int btask = std::max(8, nb - 5 - task_bits);
   int B = p->opts.chunk_log2 > 0 ? p->opts.chunk_log2 : std::min(std::min(bcap, btask), std::max(0, nb - 5));
   // exact reseed interval (perm_opts.reseed_log2): every chunk is seeded
@@ -385,7 +388,7 @@ uint64_t Planner::geometry(int K, KernelSpec& sp, int bcap) const {
   uint64_t M = p->opts.task_chunks > 0 ? (uint64_t)p->opts.task_chunks : 0;
   if (M == 0) {
     M = 1;
-    while (warp_chunks / (M * 2) >= (1ull << 17)) M *= 2;
+    while (warp_chunks / (M * 2) >= (1ull << task_bits)) M *= 2;
   }
   if (M > warp_chunks) M = warp_chunks;
   sp.n = n;
@@ -554,7 +557,6 @@ std::vector<int> Planner::elimination_search(int base, const std::vector<int>& r
     std::vector<int> c = costsort_swept(p->ccs, factored_columns(cp, s, k), k);
     Csx o = permute_ccs(p->ccs, rp, c);
     KernelSpec sp;
-    static const int score_b = getenv("PERM_SCORE_B") ? atoi(getenv("PERM_SCORE_B")) : 8;
     geometry(k, sp, score_b);
     const int sc = ev % 3;  // scoring; (ev / 3) % 2: greedy (0) or beam (1); ev / 6: composite bound tier
     sp.U = std::min(sp.U, sc == 2 ? 3 : 4);
