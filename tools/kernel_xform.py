@@ -153,6 +153,29 @@ def xf_kcase(src, scope="cases"):
     return out.replace('extern "C"', decl + 'extern "C"', 1)
 
 
+def xf_kseed(src):
+    """seed-region literals (executed once per chunk) -> a __constant__ table
+    indexed with a loop-variant zero (m & (task_stride >> 40)): an LDC.64 per
+    literal instead of two UMOVs, and a shorter seed for the instruction cache."""
+    L = src.split("\n")
+    mi = next(i for i, l in enumerate(L) if "for (unsigned m = 0;" in l)
+    li = next(i for i, l in enumerate(L) if "for (unsigned blk" in l)
+    lits = {}
+
+    def rep(m):
+        t = m.group(1)
+        a = t.lstrip("-")
+        if a not in lits:
+            lits[a] = len(lits)
+        return f"({'-' if t.startswith('-') else ''}kss_[{lits[a]} + zs_])"
+    for i in range(mi + 1, li):
+        L[i] = LIT.sub(rep, L[i])
+    L.insert(mi + 1, "      const unsigned zs_ = m & (unsigned)(task_stride >> 40);")
+    out = "\n".join(L)
+    decl = "__constant__ double kss_[%d] = {%s};\n" % (max(1, len(lits)), ", ".join(lits) or "0")
+    return out.replace('extern "C"', decl + 'extern "C"', 1)
+
+
 def xf_pipej(src):
     """software-pipelined block dispatch: j and s of the NEXT block (BREV/FLO,
     shifts: MIO latency) are computed before the current block's body, so the
@@ -454,7 +477,7 @@ VARIANTS = {"base": (lambda s: s, 128), "hot2": (xf_hot, 128), "hot2c16": (lambd
             "alap": (lambda s: xf_order(s, "alap"), 128), "dfs": (lambda s: xf_order(s, "dfs"), 128),
             "greedy": (lambda s: xf_order(s, "greedy"), 128), "rand1": (lambda s: xf_order(s, "rand", 1), 128),
             "rand2": (lambda s: xf_order(s, "rand", 2), 128), "rand3": (lambda s: xf_order(s, "rand", 3), 128), "pipej": (xf_pipej, 128), "kcase": (xf_kcase, 128), "kall": (lambda s: xf_kcase(s, "all"), 128), "un2": (xf_un2, 128), "ro": (xf_ro, 128), "ro_hot2": (lambda s: xf_ro(xf_hot(s)), 128),
-            "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64),
+            "ro_lb3": (lambda s: xf_ro(xf_lb(s, 3)), 128), "vol_hot2": (lambda s: xf_vol(xf_hot(s)), 128), "kc": (xf_kc, 128), "b64": (xf_b64, 64), "kc_b64": (lambda s: xf_b64(xf_kc(s)), 64), "kseed": (xf_kseed, 128),
             **{"ro%d" % k: (lambda s, k=k: xf_ro_le(s, k), 128) for k in (0, 3, 5, 6, 10, 12, 35)}}
 
 
