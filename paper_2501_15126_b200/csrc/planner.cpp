@@ -296,7 +296,9 @@ class Planner {
   int nvar = 1;                  // swept-column variants: 0 = base order, 1 = sorted by flip cost (AUTO only)
   std::vector<std::vector<int>> row_cols;
   int elim_cands = 6;
-  int elim_maxsize = 96, elim_maxsize_big = 160, elim_maxsize_huge = 256;
+  int elim_maxsize = 96, elim_maxsize_big = 160, elim_maxsize_huge = 256, elim_maxsize_giant = 640;
+  bool elim_tier4 = false;       // a fourth composite-bound tier (ev / 6 = 3)
+  int giant_beam = 4;            // its beam width
   int elim_beam = 4;
   bool dbg_plan = false;
   int task_bits = 17;            // floor of the warp-task count, log2 (geometry)
@@ -352,6 +354,20 @@ Planner::Planner(perm_plan_s* plan, perm_ordering ord_, double gr_, const std::s
   // larger composite-bound tiers (ev / 6 = 1, 2): real (FP64, INT01) 160 / 256, complex 64 / 96
   elim_maxsize_big = cplx_mode ? 64 : 160;
   elim_maxsize_huge = cplx_mode ? 96 : 256;
+  elim_maxsize_giant = cplx_mode ? 160 : 640;
+  // real FP64: a fourth, "giant" composite tier (640 leaf evaluations; beam
+  // searches with scorings 0 and 1 only).  B200, model picks: n=40 p=0.2
+  // 7.50 -> 6.71 ms (K=9 U=4, W 0.2239 -> 0.1971), band n=44 0.99 -> 0.75 ms,
+  // ER n=48 6.0 -> 5.4 s, n=40 seed 2 -14 %, n=36 seed 2 -12 %
+  // (profiles/r2_spill_policy_ab.jsonl); it roughly doubles the search time
+  elim_tier4 = getenv("PERM_ELIM_TIER4") ? atoi(getenv("PERM_ELIM_TIER4")) == 1 : fp64_real;
+  giant_beam = getenv("PERM_GIANT_BEAM") ? std::max(1, atoi(getenv("PERM_GIANT_BEAM"))) : 4;
+  // experiment knob: real FP64 tiers shifted up to 160 / 256 / 640
+  if (fp64_real && getenv("PERM_ELIM_SHIFT") && atoi(getenv("PERM_ELIM_SHIFT")) == 1 && !getenv("PERM_ELIM_MAXSIZE")) {
+    elim_maxsize = 160;
+    elim_maxsize_big = 256;
+    elim_maxsize_huge = 640;
+  }
   // beam width of the elimination searches (FP64: 4, INT01 / complex: greedy)
   elim_beam = std::max(1, getenv("PERM_ELIM_BEAM") ? atoi(getenv("PERM_ELIM_BEAM")) : (cplx_mode ? 1 : 4));
   dbg_plan = getenv("PERM_DEBUG_PLAN") != nullptr;
@@ -620,7 +636,8 @@ std::vector<int> Planner::elimination_search(int base, const std::vector<int>& r
         if (!seen.insert(key).second) continue;
         // bound the composite factors' evaluation size (code size, registers)
         if (elim_eval_size(p->ccs, factored_columns(cp, s2, k + 1), k + 1) >
-            (ev >= 12 ? elim_maxsize_huge : (ev >= 6 ? elim_maxsize_big : elim_maxsize)))
+            (ev >= 18 ? elim_maxsize_giant
+                      : (ev >= 12 ? elim_maxsize_huge : (ev >= 6 ? elim_maxsize_big : elim_maxsize))))
           continue;
         jobs.emplace_back(s2, std::async(std::launch::async, evalW, s2));
       }
@@ -631,7 +648,7 @@ std::vector<int> Planner::elimination_search(int base, const std::vector<int>& r
     std::sort(next.begin(), next.end());
     if (!(next[0].first < best.first * 0.995)) break;  // no further gain
     best = next[0];
-    const int width = (ev % 6) >= 3 ? elim_beam : 1;
+    const int width = (ev % 6) >= 3 ? (ev >= 18 ? giant_beam : elim_beam) : 1;
     if ((int)next.size() > width) next.resize(width);
     beam.swap(next);
   }
@@ -897,7 +914,8 @@ void Planner::search() {
   // FP64 also repeats every search with larger composite bounds (160 and 256
   // leaf evaluations): larger composites win on some matrices and lose on others
   const bool tiers = !getenv("PERM_ELIM_MAXSIZE");  // every mode: FP64, INT01, complex
-  const int nev = getenv("PERM_ELIM_VARIANTS") ? std::max(1, atoi(getenv("PERM_ELIM_VARIANTS"))) : (tiers ? 18 : 6);
+  const int nev = getenv("PERM_ELIM_VARIANTS") ? std::max(1, atoi(getenv("PERM_ELIM_VARIANTS")))
+                                                : (tiers ? (elim_tier4 ? 24 : 18) : 6);
   {
     Nvtx r_search("perm_plan/search");
     std::vector<std::pair<int, std::future<std::vector<int>>>> runs;  // greedy runs, concurrently
@@ -905,6 +923,11 @@ void Planner::search() {
       for (int ev = 0; ev < nev; ++ev) {
         if (ev % 3 == 1 && !fp64) continue;
         if ((ev / 3) % 2 == 1 && elim_beam == 1) continue;  // greedy only: the beam run would repeat it
+        // the giant composite tier (ev 18-23) only as beam searches with
+        // scorings 0 and 1 (ev 21, 22): every measured winner of that tier
+        // came from them, and its searches are the most expensive
+        if (ev >= 18 && ev != 21 && ev != 22 && !(getenv("PERM_ELIM_TIER4_ALL") && atoi(getenv("PERM_ELIM_TIER4_ALL")) == 1))
+          continue;
         runs.emplace_back(base * 32 + ev, std::async(std::launch::async, [&, base, ev] {
                             std::vector<int> rp, cp;
                             order_with(base, rp, cp);
@@ -984,8 +1007,8 @@ void Planner::rank_candidates() {
   if (getenv("PERM_DEBUG_TIMING")) fprintf(stderr, "[timing] candidates %.3f ms (%zu)\n", now_ms() - tc, cands.size());
   if (dbg_plan)
     for (const Cand& c : cands)
-      fprintf(stderr, "[plan] cand score %.5f w %.5f base %d K %d var %d bcap %d est %d cc %d pskip %.3f\n", c.score, c.w,
-              c.base, c.K, c.var, c.bcap, c.est, (int)c.cc, c.pskip);
+      fprintf(stderr, "[plan] cand score %.5f w %.5f base %d K %d var %d bcap %d est %d cc %d pskip %.3f ev %d\n", c.score, c.w,
+              c.base, c.K, c.var, c.bcap, c.est, (int)c.cc, c.pskip, c.ev);
   {  // the top ncomp by model score, plus the best of every swept-order
      // variant not among them (the model's skip / occupancy estimates are
      // rough; autotune compares the variants on the device)

@@ -476,7 +476,7 @@ static int plan_impl(int n, perm_format fmt, const int32_t* ptr, const int32_t* 
                           // codegen post-pass knobs (codegen.cpp post_pass)
                           "PERM_NO_SMEM", "PERM_SMEM_ALL", "PERM_NO_DCE", "PERM_NO_FUSE", "PERM_NO_KC", "PERM_KC_CAP", "PERM_SMEM_VOL_FRAC", "PERM_LADDER_RUNGS",
                           "PERM_NO_ASM_MUL", "PERM_ASM_MUL", "PERM_PIPE_DISPATCH", "PERM_SPILL_OK", "PERM_SCORE_B",
-                          "PERM_TASK_BITS", "PERM_NO_SMEM_RO", "PERM_SMEM_RO", "PERM_SMEM_RO_FORCE"}) {
+                          "PERM_TASK_BITS", "PERM_NO_SMEM_RO", "PERM_SMEM_RO", "PERM_SMEM_RO_FORCE", "PERM_ELIM_TIER4", "PERM_ELIM_SHIFT", "PERM_GIANT_BEAM", "PERM_ELIM_TIER4_ALL"}) {
       const char* v = getenv(k);
       pkey += k;
       pkey += '=';

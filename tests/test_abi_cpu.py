@@ -380,6 +380,7 @@ def test_plan_export_import_keeps_spilling_smem_ro_kernel(monkeypatch):
     frame in local_bytes."""
     monkeypatch.setenv("PERM_SMEM_RO_FORCE", "1")
     monkeypatch.setenv("PERM_SPILL_OK", "4096")
+    monkeypatch.setenv("PERM_ELIM_TIER4", "0")  # the plan this fixture was chosen on
     A = synth.erdos_renyi(22, 0.3, 2)
     P = pb.Plan.from_dense(A, mode="reg", block_log2=5, no_device=True, autotune=-1)
     assert P.info["local_bytes"] > 0 and "volatile double" in P.source
@@ -454,3 +455,18 @@ def test_empty_column_is_singular_without_planning():
         assert P.info["singular"] == 1 and P.info["struct_rank"] == 17
         assert P.info["row_perm"] == list(range(18)) and P.info["K"] == 0
         P.close()
+
+
+def test_checkpoint_auto_pieces_keep_many_waves():
+    """checkpoint.auto_pieces: power-of-two pieces of >= 2^14 warp-tasks each
+    (~14 waves of a B200's resident warps), at most 128, at least 1."""
+    from paper_2501_15126_b200.checkpoint import auto_pieces, MIN_TASKS_PER_PIECE
+    big = pb.Plan.from_dense(synth.erdos_renyi(40, 0.2, 1), mode="reg", no_device=True, autotune=-1)
+    small = pb.Plan.from_dense(synth.erdos_renyi(20, 0.3, 1), mode="reg", no_device=True, autotune=-1)
+    for P in (big, small):
+        k = auto_pieces(P)
+        t = P.info["tasks"]
+        assert k & (k - 1) == 0 and 1 <= k <= 128
+        assert k == 1 or t // k >= MIN_TASKS_PER_PIECE
+        assert k == 128 or t // (2 * k) < MIN_TASKS_PER_PIECE
+    assert auto_pieces(big) == 8 and auto_pieces(small) == 1

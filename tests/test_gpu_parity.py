@@ -678,6 +678,7 @@ def test_spilling_and_smem_ro_kernels_vs_oracle(n, p, seed, uses, monkeypatch):
     monkeypatch.setenv("PERM_SMEM_RO", str(uses))
     monkeypatch.setenv("PERM_SMEM_RO_FORCE", "1")
     monkeypatch.setenv("PERM_SPILL_OK", "4096")
+    monkeypatch.setenv("PERM_ELIM_TIER4", "0")  # the plans these fixtures were chosen on
     A = synth.erdos_renyi(n, p, seed)
     exp, _ = oracle.perm_nw(A)
     for kw in ({"autotune": -1}, {}):

@@ -31,7 +31,7 @@ def main():
         if os.path.exists(ck):
             os.remove(ck)
         t0 = time.perf_counter()
-        r = compute_resumable(P, ck, pieces=64)
+        r = compute_resumable(P, ck)  # auto_pieces: >= 2^14 warp-tasks per piece
         wall = time.perf_counter() - t0
         sweep = 0.0
         import json as _j

@@ -51,7 +51,7 @@ def main():
     # DESIGN 3.13(f): a spilling FP64 kernel that reads body values from
     # volatile shared-memory slots (the smem_ro rung, forced), and a spilling
     # INT01 kernel (accepted under autotune in production)
-    os.environ.update(PERM_SMEM_RO_FORCE="1", PERM_SPILL_OK="4096")
+    os.environ.update(PERM_SMEM_RO_FORCE="1", PERM_SPILL_OK="4096", PERM_ELIM_TIER4="0")
     C = synth.erdos_renyi(22, 0.3, 2)
     P = pb.Plan.from_dense(C, mode="reg", block_log2=5, autotune=-1)
     assert P.info["local_bytes"] > 0 and "volatile double" in P.source
@@ -65,6 +65,7 @@ def main():
     assert Q.exact() == oracle.perm_nw_exact(D)
     print("ok int01 spill", Q.info["local_bytes"], flush=True)
     del os.environ["PERM_SPILL_OK"]
+    del os.environ["PERM_ELIM_TIER4"]
     # the bench plan (n=40, K=8 B=8 U=5, 48-byte frame): one 1/128 shard
     E = synth.erdos_renyi(40, 0.2, 1)
     P = pb.Plan.from_dense(E, mode="reg", autotune=-1)
