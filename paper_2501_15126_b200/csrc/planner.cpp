@@ -858,14 +858,14 @@ Built Planner::build(const Cand& c) {
     return (t.stack <= spill_ok && t.spill <= spill_ok) || getenv("PERM_ALLOW_SPILL");
   };
   // the first rungs compile concurrently (speculatively); the first
-  // spill-free rung in ladder order wins -- the same choice as compiling
-  // them one after another, in one compile latency
-  // (two speculative rungs: the first spill-free rung was the first or
-  // second in every measured plan, and the extra rungs only compete for
-  // host cores with the other candidates' compiles)
+  // accepted rung in ladder order wins -- the same choice as compiling
+  // them one after another, in one compile latency.  Real FP64 speculates
+  // four (U, U + smem_ro, U-1, U-1 + smem_ro: the n=40 bench plan is taken
+  // at the fourth), other modes two (the first spill-free rung was the
+  // first or second in every measured plan)
   std::vector<std::pair<KernelSpec, uint64_t>> ladder = {{b.sp, b.tasks}};
   const size_t spec_rungs = getenv("PERM_LADDER_RUNGS") ? (size_t)std::max(1, atoi(getenv("PERM_LADDER_RUNGS")))
-                                                        : (smem_ro_rung ? 3 : 2);
+                                                        : (smem_ro_rung ? 4 : 2);
   while (ladder.size() < spec_rungs) {
     auto nx = ladder.back();
     if (!escalate(nx.first, nx.second)) break;
