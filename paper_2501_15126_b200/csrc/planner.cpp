@@ -338,7 +338,10 @@ Planner::Planner(perm_plan_s* plan, perm_ordering ord_, double gr_, const std::s
   // spill (K=8 U=3) runs 9.9 ms against 12.7 ms spill-free, while the model
   // alone would pick a slower spilling kernel (16.1 ms, profiles/r2_spill_policy_ab.jsonl)
   const bool i01_measured = mode == PERM_MODE_INT01 && will_autotune;
-  spill_ok = getenv("PERM_SPILL_OK") ? atoi(getenv("PERM_SPILL_OK")) : ((fp64_real || i01_measured) ? 64 : 0);
+  // real FP64 96 bytes: with the giant tier the n=40 plan's U-1 rung keeps an
+  // 88-byte frame and runs 6.42 ms against 6.70 ms for its spill-free
+  // smem_ro rung; no FP64 config was slower at 96 than at 64
+  spill_ok = getenv("PERM_SPILL_OK") ? atoi(getenv("PERM_SPILL_OK")) : (fp64_real ? 96 : (i01_measured ? 64 : 0));
   spill_pen = mode == PERM_MODE_INT01 ? 1.3 : 1.04;
   smem_ro_rung = fp64_real && !(getenv("PERM_NO_SMEM_RO") && atoi(getenv("PERM_NO_SMEM_RO")) == 1);
   smem_ro_uses = getenv("PERM_SMEM_RO") ? std::max(1, atoi(getenv("PERM_SMEM_RO"))) : 6;

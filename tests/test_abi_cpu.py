@@ -137,12 +137,12 @@ def test_no_device_plan_then_compute_fails_loudly():
 @pytest.mark.parametrize("n,p,seed,mode", [(10, 0.3, 1, "auto"), (30, 0.3, 1, "reg"), (36, 0.2, 1, "reg"),
                                            (40, 0.2, 1, "reg"), (40, 0.2, 2, "reg"), (12, 0.3, 3, "int01")])
 def test_codegen_compiles_within_spill_tolerance(n, p, seed, mode):
-    """Real FP64 accepts a local frame of <= 64 bytes per thread (DESIGN
-    3.13(f)); INT01 and complex kernels stay spill-free."""
+    """Real FP64 accepts a local frame of <= 96 bytes per thread (DESIGN
+    3.13(f)); INT01 (without autotune) and complex kernels stay spill-free."""
     A = synth.erdos_renyi(n, p, seed, binary=(mode == "int01"))
     P = pb.Plan.from_dense(A, ordering="auto", mode=mode, no_device=True)
     i = P.info
-    assert i["local_bytes"] <= (0 if i["mode"] == 3 else 64)
+    assert i["local_bytes"] <= (0 if i["mode"] == 3 else 96)
     assert 0 < i["regs_per_thread"] <= 255
     assert i["w_plan"] > 0
     assert "perm_sweep" in P.source
@@ -322,7 +322,7 @@ def test_maximum_size_n64_plans_full_gray_range():
     A = synth.givens_brickwork(64, 4, 1)
     P = pb.Plan.from_dense(A, mode="reg", no_device=True)
     i = P.info
-    assert i["local_bytes"] <= 64 and i["w_plan"] > 0
+    assert i["local_bytes"] <= 96 and i["w_plan"] > 0
     assert i["tasks"] & (i["tasks"] - 1) == 0
     steps = i["tasks"] * 32 * i["M"] * (1 << i["B"]) * (1 << i["K"])
     assert steps == 2 ** 63
@@ -330,12 +330,14 @@ def test_maximum_size_n64_plans_full_gray_range():
     assert r[-1] == 2 ** 63
 
 
-def test_smem_placement_of_values_the_body_never_touches():
+def test_smem_placement_of_values_the_body_never_touches(monkeypatch):
     """DESIGN 3.13(d): loop-carried values absent from the block body live in
     per-thread shared-memory slots; none of them appears in the body.
     DESIGN 3.13(f): the spill-escalation rung (the n=40 bench plan takes it)
     also places values the body only reads, at most 6 times, in volatile
-    slots: those appear in the body as reads only."""
+    slots: those appear in the body as reads only (at a 64-byte tolerance the
+    n=40 plan takes that rung; at the default 96 a plain 88-byte frame wins)."""
+    monkeypatch.setenv("PERM_SPILL_OK", "64")
     A = synth.erdos_renyi(40, 0.2, 1)
     P = pb.Plan.from_dense(A, mode="reg", no_device=True, autotune=-1)
     src, i = P.source, P.info
