@@ -272,23 +272,31 @@ def run_reference(args, rank, world):
           "e2e": {"value": value, "unit": "Gray-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
 
-def audited_kernel(info):
+def kernel_sha(source: str) -> str:
+    import hashlib
+    return hashlib.sha256(source.encode()).hexdigest()[:16]
+
+
+def audited_kernel(info, source):
     """ncu-audited executed DP instructions per Gray step and DRAM traffic per
     launch of this exact kernel, from the committed `ncu` captures under
-    profiles/ (matched on the plan signature), else None."""
+    profiles/ (matched on the plan signature AND the generated source's hash:
+    two kernels of the same geometry and W_plan can differ, e.g. in their
+    shared-memory placement, and execute different DP counts), else None."""
     import glob
     sig = {k: info[k] for k in ("n", "nnz", "K", "B", "U", "M", "tasks", "w_plan")}
+    sha = kernel_sha(source)
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernel_ncu.json")), reverse=True):
         for t in json.load(open(path)).get("entries", []):
-            if t.get("signature") == sig:
+            if t.get("signature") == sig and t.get("kernel_sha") == sha:
                 return t
     return None
 
 
-def roofline(info, sweep_ms, gray_per_launch, peak, peak_def, peak_nominal):
+def roofline(info, sweep_ms, gray_per_launch, peak, peak_def, peak_nominal, source):
     """Roofline of the sweep kernel: FP64 lane-ops (DADD/DMUL/DFMA thread
     instructions) per launch / launch time, against the FP64 lane peak."""
-    aud = audited_kernel(info)
+    aud = audited_kernel(info, source)
     w_ops, w_src = info["w_plan"], "generator count (W_plan)"
     traffic, traffic_src = None, None
     if aud:
@@ -541,7 +549,7 @@ def main():
                         f"{info['sms']} SMs x 64 FP64 lanes x {sm_max:.0f} MHz = {peak_nominal:.3f}")
         except Exception as e:  # noqa: BLE001
             peak, peak_def = peak_nominal, f"nominal {info['sms']} SMs x 64 FP64 lanes x {sm_max:.0f} MHz (probe failed: {e})"
-        rf = roofline(info, sw, products, peak, peak_def, peak_nominal)
+        rf = roofline(info, sw, products, peak, peak_def, peak_nominal, plan.source)
         rel_err, golden = golden_rel_err(args, result)
         line = {
             "metric": "gray_steps_per_s", "value": value, "unit": "Gray-steps/s", "n_gpus": world,
@@ -587,7 +595,7 @@ def main():
             P0, pms, psweep = plain
             i0 = P0.info
             psw = sum(psweep) / len(psweep)
-            prf = roofline(i0, psw, gray_per_launch(i0), peak, peak_def, peak_nominal)
+            prf = roofline(i0, psw, gray_per_launch(i0), peak, peak_def, peak_nominal, P0.source)
             pms_avg = sum(pms) / len(pms)
             line["plain_sweep"] = {
                 "what": "the literal Alg. 1 loop (P:86-115) on the same matrix: Alg. 3 ordering, factor_cols=-1 "

@@ -54,6 +54,8 @@ def signature(name):
     make, kw, order = WORKLOADS[name]
     P = pb.Plan.from_dense(make(synth), order, no_device=True, **kw)
     i = P.info
+    import hashlib
+    i = dict(i, kernel_sha=hashlib.sha256(P.source.encode()).hexdigest()[:16])
     P.close()
     return {k: i[k] for k in ("n", "nnz", "K", "B", "U", "M", "tasks", "w_plan")}, i
 
@@ -102,7 +104,7 @@ def main():
         k = ks[0]
         sig, info = signature(name)
         gray = info["tasks"] * 32 * info["M"] * (1 << info["B"]) * (1 << info["K"])
-        e = {"workload": name, "signature": sig,
+        e = {"workload": name, "signature": sig, "kernel_sha": info["kernel_sha"],
              "dram_bytes_per_launch": num(k["dram__bytes_read.sum"]) + num(k["dram__bytes_write.sum"]),
              "source": f"profiles/{a.round}_ncu_summary.md (ncu --set full, {rep})",
              "fp64_pipe_pct": num(k["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]),
